@@ -1,0 +1,252 @@
+/*
+ * spmvb.h — C ABI of the B200-native fp64 SpMV library (libspmvb.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `spmvkit` (arXiv 1805.11938 artifact, /root/reference/pkg/src/spmvkit).
+ * The reference is pure Python, so its "FFI" is its Python function surface;
+ * each entry point below names the reference function it replaces
+ * (file:line relative to /root/reference/pkg/src/spmvkit/).  The Python
+ * binding that a maintainer would add is shown in INTEGRATION.md and is
+ * implemented by paper_1805_11938_b200/_lib.py (ctypes).
+ *
+ * Conventions
+ *  - Every function is extern "C", reentrant, and stream-ordered on the
+ *    `stream` argument (a cudaStream_t passed as void*; NULL = legacy
+ *    default stream).  Device pointers are caller-allocated unless noted.
+ *  - Indices are int32 (the reference stores int64 with a 32-bit range
+ *    contract, coo.py:37-38; the byte model assumes 4-byte indices,
+ *    bench.py:13-14).  Row pointers are int32, so nnz < 2^31.
+ *  - Values are IEEE fp64.
+ *  - Return value: SPMVB_OK or an error status; the message for the last
+ *    failure on the calling thread is returned by spmvb_last_error().
+ *  - Functions whose output size depends on the data are split into a
+ *    *_begin / *_plan step that returns the size (synchronizing the stream)
+ *    and a *_finish / fill step that writes caller-allocated outputs.
+ *  - Temporaries are allocated stream-ordered (cudaMallocAsync).
+ *  - No CPU fallback exists: every compute entry point launches CUDA kernels.
+ */
+#ifndef SPMVB_H_
+#define SPMVB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to Python exceptions by _lib.py) ------------- */
+#define SPMVB_OK 0
+#define SPMVB_INVALID_ARG 1     /* ValueError                                  */
+#define SPMVB_GRID_TOO_LARGE 2  /* ConversionError (formats.py:61-62)          */
+#define SPMVB_OUT_OF_RANGE 3    /* ValueError "... is outside ..." (coo.py:108-115) */
+#define SPMVB_CUDA_ERROR 4      /* RuntimeError                                */
+#define SPMVB_OUT_OF_MEMORY 5   /* MemoryError                                 */
+#define SPMVB_INTERNAL 6        /* RuntimeError                                */
+
+#define SPMVB_ABI_VERSION 1
+
+const char* spmvb_last_error(void);
+int spmvb_abi_version(void);
+
+/* ======================================================================== */
+/* COO core — replaces coo.py                                               */
+/* ======================================================================== */
+
+typedef struct spmvb_canon spmvb_canon;
+
+/* canonicalize (coo.py:86-125), phase 1.  Sorts (row, col) stably, sums
+ * duplicates in numpy reduceat order (first + pairwise(rest)) and drops sums
+ * equal to 0.0.  row/col are int32 (index_width 4) or int64 (index_width 8)
+ * device arrays.  On an out-of-bounds entry returns SPMVB_OUT_OF_RANGE and
+ * writes bad[0..2] = {first bad entry index, its row, its col} (host array).
+ * On success *nnz_out (host) holds the canonical nnz and *plan must be passed
+ * to spmvb_canonicalize_finish (or spmvb_canonicalize_free).  The input
+ * arrays must stay alive until finish. */
+int spmvb_canonicalize_begin(const void* row, const void* col, int index_width, const double* val,
+                             int64_t nnz_in, int64_t n_rows, int64_t n_cols, spmvb_canon** plan,
+                             int64_t* nnz_out, int64_t* bad, void* stream);
+int spmvb_canonicalize_finish(spmvb_canon* plan, int32_t* row_out, int32_t* col_out, double* val_out,
+                              void* stream);
+void spmvb_canonicalize_free(spmvb_canon* plan);
+
+/* row_nnz_histogram (coo.py:144-146) on canonical (row-sorted) COO. */
+int spmvb_row_nnz_histogram(const int32_t* row, int64_t nnz, int64_t n_rows, int64_t* counts_out,
+                            void* stream);
+
+/* dense_spmv_oracle (coo.py:128-141): y_i accumulated entry by entry in
+ * ascending (row, col) order with separately rounded products (no FMA);
+ * bit-identical to the reference oracle. ptr is the CSR row pointer. */
+int spmvb_spmv_sequential(int64_t n_rows, const int32_t* ptr, const int32_t* col, const double* val,
+                          const double* x, double* y, void* stream);
+
+/* ======================================================================== */
+/* Formats — replaces formats.py                                            */
+/* ======================================================================== */
+
+/* to_csr (formats.py:183-188): ptr[n_rows+1] from row-sorted COO rows;
+ * col/val copied (the reference returns new arrays). */
+int spmvb_coo_to_csr(const int32_t* row, const int32_t* col, const double* val, int64_t nnz,
+                     int64_t n_rows, int32_t* ptr_out, int32_t* col_out, double* val_out, void* stream);
+
+/* Row-length statistics from a CSR ptr (host output):
+ * out[0] = min count, out[1] = max count, out[2] = number of non-empty rows. */
+int spmvb_csr_row_stats(const int32_t* ptr, int64_t n_rows, int64_t* out3, void* stream);
+
+/* to_csr5 (formats.py:196-250).  num_tiles = ceil(nnz/(omega*sigma)).
+ * Outputs (device): tile_ptr[num_tiles+1], bit_flag[nnz] (uint8, stored
+ * order), y_off[num_tiles*omega], seg_off[num_tiles*omega] (int32, row-major
+ * (tile, column)), col_out[nnz], val_out[nnz] (stored order).
+ * Also writes the kernel's auxiliary per-tile word tile_aux[num_tiles]
+ * (bit 31: the tile head continues a row begun in an earlier tile; bits 0-30:
+ * rank of tile_ptr[t] among non-empty rows).  SPMVB_INVALID_ARG if omega < 1
+ * or sigma < 1 (message names omega/sigma as the reference does). */
+int spmvb_csr_to_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
+                      int omega, int sigma, int32_t* tile_ptr, uint8_t* bit_flag, int32_t* y_off,
+                      int32_t* seg_off, int32_t* col_out, double* val_out, uint32_t* tile_aux, void* stream);
+
+/* List of non-empty rows (ascending) used by the CSR5 kernel when empty rows
+ * exist; rows_out has `nonempty` entries (from spmvb_csr_row_stats). */
+int spmvb_csr_nonempty_rows(const int32_t* ptr, int64_t n_rows, int32_t* rows_out, void* stream);
+
+/* to_ell (formats.py:281-288 via _padded_grids :253-278).  Grid stored
+ * column-major: element (r, j) at j*n_rows + r.  Pads repeat the row's last
+ * valid column (0 for an empty row) with value 0.0.  SPMVB_GRID_TOO_LARGE
+ * (checked before any write) if n_rows*k > max_cells. Writes row_nnz. */
+int spmvb_csr_to_ell(int64_t n_rows, const int32_t* ptr, const int32_t* col, const double* val, int64_t k,
+                     int64_t max_cells, int32_t* idx_out, double* val_out, int64_t* row_nnz_out, void* stream);
+
+/* to_sell (formats.py:291-344), phase 1: permutation, slice widths, slice
+ * offsets (in cells) and permuted row counts; *total_cells (host) returned.
+ * SPMVB_INVALID_ARG for c < 1 or sigma not in {0} U cN ("multiple");
+ * SPMVB_GRID_TOO_LARGE if total cells > max_cells.  Arrays: perm[n_rows],
+ * widths[S], slice_off[S+1] (int64), row_nnz_perm[n_rows]; S = ceil(n/c). */
+int spmvb_sell_plan(int64_t n_rows, const int32_t* ptr, int64_t c, int64_t sigma, int64_t max_cells,
+                    int32_t* perm, int64_t* widths, int64_t* slice_off, int64_t* row_nnz_perm,
+                    int64_t* total_cells, void* stream);
+/* Phase 2: fill the per-slice column-major grids into flat arrays. */
+int spmvb_sell_fill(int64_t n_rows, const int32_t* ptr, const int32_t* col, const double* val, int64_t c,
+                    const int32_t* perm, const int64_t* widths, const int64_t* slice_off, int32_t* idx_out,
+                    double* val_out, void* stream);
+
+/* hyb_typical_k (formats.py:347-358) on a CSR ptr; *k_out (host). */
+int spmvb_hyb_typical_k(const int32_t* ptr, int64_t n_rows, int64_t* k_out, void* stream);
+/* hyb_typical_k on an int64 per-row count array (device). */
+int spmvb_typical_k_counts(const int64_t* counts, int64_t n, int64_t* k_out, void* stream);
+/* to_hyb (formats.py:361-397), phase 1: tail_ptr[n_rows+1] (exclusive scan of
+ * max(count-K,0)); *tail_nnz (host). */
+int spmvb_hyb_plan(int64_t n_rows, const int32_t* ptr, int64_t k, int64_t max_cells, int32_t* tail_ptr,
+                   int64_t* tail_nnz, void* stream);
+/* Phase 2: ELL part (column-major, pads = last kept col) with row_nnz =
+ * min(count, K), and the canonical-order COO tail. */
+int spmvb_hyb_fill(int64_t n_rows, const int32_t* ptr, const int32_t* col, const double* val, int64_t k,
+                   const int32_t* tail_ptr, int32_t* ell_idx, double* ell_val, int64_t* ell_row_nnz,
+                   int32_t* tail_row, int32_t* tail_col, double* tail_val, void* stream);
+
+/* ---- to_coo (formats.py:400-453): triplet extraction; the Python layer
+ *      passes the triplets through spmvb_canonicalize_* as the reference
+ *      passes them through canonicalize. ------------------------------------ */
+/* rows_out[k] = row of CSR position k. */
+int spmvb_csr_expand_rows(const int32_t* ptr, int64_t n_rows, int32_t* rows_out, void* stream);
+/* Undo the CSR5 stored order: col/val in stored order -> CSR order. */
+int spmvb_csr5_unstore(int64_t nnz, int omega, int sigma, const int32_t* col, const double* val, int32_t* col_out,
+                       double* val_out, void* stream);
+/* ELL grid (column-major) -> triplets in row-major order, first row_nnz[r]
+ * slots per row; outputs sized sum(row_nnz). */
+int spmvb_ell_to_coo(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const int64_t* row_nnz,
+                     int32_t* rows_out, int32_t* cols_out, double* vals_out, void* stream);
+/* SELL slices -> triplets in permuted-row order (not canonical). */
+int spmvb_sell_to_coo(int64_t n_rows, int64_t c, const int32_t* perm, const int64_t* slice_off,
+                      const int64_t* row_nnz_perm, const int32_t* idx, const double* val, int32_t* rows_out,
+                      int32_t* cols_out, double* vals_out, void* stream);
+
+/* ======================================================================== */
+/* SpMV kernels — replaces kernels.py (y = scale * A x).                    */
+/* `scale` is an optional device scalar (NULL = 1.0) multiplying each row   */
+/* result; power iteration uses it for deferred normalisation.              */
+/* Results are deterministic (no floating-point atomics).                   */
+/* ======================================================================== */
+
+/* Analysis for the merge-path CSR kernel (like a cuSPARSE buffer): per-tile
+ * merge coordinates tile_row[num_tiles+1], tile_nz[num_tiles+1] with
+ * num_tiles = spmvb_csr_merge_tiles(n_rows, nnz). */
+int64_t spmvb_csr_merge_tiles(int64_t n_rows, int64_t nnz);
+int spmvb_csr_merge_plan(int64_t n_rows, int64_t nnz, const int32_t* ptr, int32_t* tile_row, int32_t* tile_nz,
+                         void* stream);
+
+/* spmv_csr (kernels.py:76-95).  carry_row/carry_val: num_tiles scratch. */
+int spmvb_spmv_csr(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
+                   const int32_t* tile_row, const int32_t* tile_nz, int32_t* carry_row, double* carry_val,
+                   const double* x, double* y, const double* scale, void* stream);
+
+/* spmv_csr5 (kernels.py:139-174). nonempty_rows may be NULL when every row is
+ * non-empty. carry: num_tiles scratch doubles. */
+int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma, const int32_t* tile_ptr,
+                    const uint8_t* bit_flag, const int32_t* col, const double* val, const uint32_t* tile_aux,
+                    const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x, double* y,
+                    const double* scale, void* stream);
+
+/* spmv_ell (kernels.py:98-116): per-row sequential accumulation over all k
+ * slots (pads included), separately rounded products: bit-identical to the
+ * reference kernel. */
+int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const double* x, double* y,
+                   const double* scale, void* stream);
+
+/* spmv_sell (kernels.py:119-136); perm may be NULL for sigma == 0. */
+int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
+                    const int32_t* perm, const int32_t* idx, const double* val, const double* x, double* y,
+                    const double* scale, void* stream);
+
+/* spmv_hyb (kernels.py:177-199): ELL part plus the COO tail, reduced through
+ * the tail's row pointer (tail_ptr from spmvb_hyb_plan) by the merge-path
+ * kernel; tile_row/tile_nz from spmvb_csr_merge_plan over (tail_ptr, tail_nnz). */
+int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const double* ell_val, int64_t tail_nnz,
+                   const int32_t* tail_ptr, const int32_t* tail_col, const double* tail_val,
+                   const int32_t* tile_row, const int32_t* tile_nz, int32_t* carry_row, double* carry_val,
+                   const double* x, double* y, const double* scale, void* stream);
+
+/* ||y||^2 over n entries into *out (device), deterministic two-level sum.
+ * Used by power iteration. */
+int spmvb_sumsq(const double* y, int64_t n, double* out, void* stream);
+/* scale_out = 1/sqrt(*sumsq) (device scalars). */
+int spmvb_inv_sqrt(const double* sumsq, double* scale_out, void* stream);
+
+/* ======================================================================== */
+/* Features — replaces features.py:69-84 (extract_features)                 */
+/* ======================================================================== */
+
+/* out8 (host): n_rows, n_cols, nnz_frac, nnz_min, nnz_max, nnz_avg, nnz_std,
+ * variation — bit-identical to numpy (mean = nnz/n_rows, population std via
+ * numpy's pairwise summation of squared deviations).  Zero-dimension input
+ * returns SPMVB_INVALID_ARG ("undefined"). */
+int spmvb_csr_features(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* ptr, double* out8,
+                       void* stream);
+/* Extra structure features kept outside FeatureVector (north star): out2
+ * (host) = {bandwidth = max |i-j| over stored entries (0 if nnz == 0),
+ * diagonal density = #{i : (i,i) stored} / min(n_rows, n_cols)}. */
+int spmvb_csr_extra_features(int64_t n_rows, int64_t n_cols, const int32_t* ptr, const int32_t* col,
+                             double* out2, void* stream);
+
+/* ======================================================================== */
+/* Synthetic inputs; not part of the reference API.          */
+/* ======================================================================== */
+
+/* R-MAT edge list: `draws` edges over a 2^scale square, quadrant
+ * probabilities (a, b, c, 1-a-b-c) per bit from a counter-based hash of
+ * (seed, draw, level); value 1 - U[0,1).  Duplicates removed keeping the first
+ * draw; survivors emitted in draw order (unsorted).  Phase 1 returns the
+ * survivor count and a plan; phase 2 writes them. */
+typedef struct spmvb_rmat spmvb_rmat;
+int spmvb_rmat_begin(int scale, int64_t draws, double a, double b, double c, uint64_t seed, spmvb_rmat** plan,
+                     int64_t* nnz_out, void* stream);
+int spmvb_rmat_finish(spmvb_rmat* plan, int32_t* row_out, int32_t* col_out, double* val_out, void* stream);
+void spmvb_rmat_free(spmvb_rmat* plan);
+
+/* Fill a device vector with U[lo, hi) from the same hash (x for benchmarks). */
+int spmvb_fill_uniform(double* x, int64_t n, double lo, double hi, uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPMVB_H_ */

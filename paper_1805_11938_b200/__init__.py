@@ -1,0 +1,58 @@
+"""B200-native fp64 SpMV library (drop-in for the hot path of spmvkit,
+the artifact of arXiv 1805.11938).
+
+Public names mirror ``spmvkit``'s hot-path API (coo, formats, kernels,
+features, select_format).  All compute runs in hand-written sm_100a CUDA
+kernels in ``libspmvb.so`` (C ABI: include/spmvb.h) loaded with ctypes; the
+package refuses to import if the library is missing (no CPU fallback).
+"""
+
+from . import _lib
+
+_lib.load()  # fail loudly at import time if libspmvb.so is missing
+
+from .coo import (  # noqa: E402
+    INDEX_LIMIT,
+    CooMatrix,
+    MatrixMarketError,
+    canonicalize,
+    coo_equal,
+    dense_spmv_oracle,
+    read_matrix_market,
+    row_nnz_histogram,
+    write_matrix_market,
+)
+from .features import (  # noqa: E402
+    FEATURE_NAMES,
+    FeatureVector,
+    ScalingParams,
+    apply_scaling,
+    extract_extra_features,
+    extract_features,
+    fit_scaling,
+)
+from .formats import (  # noqa: E402
+    DEFAULT_MAX_GRID_CELLS,
+    ConversionError,
+    Csr5Matrix,
+    CsrMatrix,
+    EllMatrix,
+    FormatMatrix,
+    FormatTag,
+    HybMatrix,
+    SellMatrix,
+    convert,
+    hyb_typical_k,
+    to_coo,
+    to_csr,
+    to_csr5,
+    to_ell,
+    to_hyb,
+    to_sell,
+)
+from . import synth  # noqa: E402
+from .harness import bandwidth_estimate, spmv_bytes, spmv_flops  # noqa: E402
+from .kernels import spmv, spmv_csr, spmv_csr5, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
+from .model import DecisionTreeModel, ModelIOError, load_model, predict, select_format  # noqa: E402
+
+__version__ = "0.1.0"

@@ -1,0 +1,378 @@
+// COO core on the GPU: canonicalize, row histogram, COO->CSR, row stats,
+// the sequential-order SpMV used as the on-device oracle, and small
+// reductions used by power iteration.
+//
+// Reference: /root/reference/pkg/src/spmvkit/coo.py:86-146, formats.py:183-188.
+#include "prims.cuh"
+
+using namespace spmvb;
+
+struct spmvb_canon {
+  int64_t n_in = 0, n_out = 0, n_rows = 0, n_cols = 0;
+  int colbits = 0;
+  int index_width = 4;
+  bool fast = false;  // input already canonical: finish is a narrowing copy
+  const void* row = nullptr;
+  const void* col = nullptr;
+  const double* val = nullptr;
+  DevBuf<uint64_t> keys_a, keys_b;
+  DevBuf<uint32_t> vals_b, vals_s;
+  uint64_t* skeys = nullptr;
+  uint32_t* sidx = nullptr;
+  DevBuf<double> sums;
+  DevBuf<uint8_t> keep;
+  DevBuf<uint32_t> pos;
+};
+
+namespace {
+
+template <typename I>
+__global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__ col, const double* __restrict__ val,
+                                int64_t n, int64_t n_rows, int64_t n_cols, int colbits, uint64_t* __restrict__ keys,
+                                unsigned long long* bad, int* noncanonical) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = static_cast<int64_t>(row[i]);
+    int64_t c = static_cast<int64_t>(col[i]);
+    bool oob = r < 0 || r >= n_rows || c < 0 || c >= n_cols;
+    uint64_t key = oob ? 0ull : ((static_cast<uint64_t>(r) << colbits) | static_cast<uint64_t>(c));
+    keys[i] = key;
+    if (oob) atomicMin(bad, static_cast<unsigned long long>(i));
+    bool nc = (val[i] == 0.0);
+    if (i > 0 && !oob) {
+      int64_t pr = static_cast<int64_t>(row[i - 1]);
+      int64_t pc = static_cast<int64_t>(col[i - 1]);
+      if (pr > r || (pr == r && pc >= c)) nc = true;
+    }
+    if (nc) atomicOr(noncanonical, 1);
+  }
+}
+
+__global__ void k_canon_runs(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,
+                             const double* __restrict__ val, int64_t n, double* __restrict__ sums,
+                             uint8_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t k = skeys[i];
+    bool head = (i == 0) || (skeys[i - 1] != k);
+    if (!head) {
+      keep[i] = 0;
+      continue;
+    }
+    int64_t e = i + 1;
+    while (e < n && skeys[e] == k) ++e;
+    double v0 = val[sidx[i]];
+    double s = v0;
+    if (e - i > 1) {
+      // numpy add.reduceat on a run: first element + pairwise(rest)
+      auto at = [&](int64_t j) { return val[sidx[j]]; };
+      s = v0 + np_pairwise(at, i + 1, e - i - 1);
+    }
+    sums[i] = s;
+    keep[i] = (s != 0.0) ? 1 : 0;  // NaN != 0.0: kept, as in coo.py:124
+  }
+}
+
+__global__ void k_canon_emit(const uint64_t* __restrict__ skeys, const double* __restrict__ sums,
+                             const uint8_t* __restrict__ keep, const uint32_t* __restrict__ pos, int64_t n,
+                             int colbits, int32_t* __restrict__ row_out, int32_t* __restrict__ col_out,
+                             double* __restrict__ val_out) {
+  const uint64_t mask = (colbits >= 64) ? ~0ull : ((1ull << colbits) - 1ull);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!keep[i]) continue;
+    uint64_t k = skeys[i];
+    uint32_t p = pos[i];
+    row_out[p] = static_cast<int32_t>(k >> colbits);
+    col_out[p] = static_cast<int32_t>(k & mask);
+    val_out[p] = sums[i];
+  }
+}
+
+template <typename I>
+__global__ void k_narrow_copy(const I* __restrict__ row, const I* __restrict__ col, const double* __restrict__ val,
+                              int64_t n, int32_t* __restrict__ row_out, int32_t* __restrict__ col_out,
+                              double* __restrict__ val_out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    row_out[i] = static_cast<int32_t>(row[i]);
+    col_out[i] = static_cast<int32_t>(col[i]);
+    val_out[i] = val[i];
+  }
+}
+
+__global__ void k_row_counts(const int32_t* __restrict__ row, int64_t nnz, unsigned int* __restrict__ counts) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i - threadIdx.x < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    bool valid = i < nnz;
+    int r = valid ? row[i] : -1;
+    unsigned peers = __match_any_sync(0xffffffffu, r);
+    if (valid && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
+      atomicAdd(&counts[r], static_cast<unsigned>(__popc(peers)));
+  }
+}
+
+__global__ void k_counts_to_i64(const unsigned int* __restrict__ c, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<int64_t>(c[i]);
+}
+
+__global__ void k_spmv_sequential(int64_t n_rows, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                  const double* __restrict__ val, const double* __restrict__ x,
+                                  double* __restrict__ y) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(val[k], x[col[k]]));
+    y[r] = acc;
+  }
+}
+
+__global__ void k_inv_sqrt(const double* sumsq, double* scale) {
+  double s = *sumsq;
+  *scale = (s > 0.0) ? 1.0 / sqrt(s) : 1.0;
+}
+
+void check_shape(int64_t n_rows, int64_t n_cols) {
+  if (n_rows < 0 || n_cols < 0) fail(SPMVB_INVALID_ARG, "negative matrix shape %lldx%lld", (long long)n_rows, (long long)n_cols);
+  if (n_rows > INT32_MAX || n_cols > INT32_MAX)
+    fail(SPMVB_INVALID_ARG, "matrix shape %lldx%lld exceeds the 32-bit index range of the GPU layout (int32)",
+         (long long)n_rows, (long long)n_cols);
+}
+
+}  // namespace
+
+extern "C" int spmvb_canonicalize_begin(const void* row, const void* col, int index_width, const double* val,
+                                        int64_t nnz_in, int64_t n_rows, int64_t n_cols, spmvb_canon** plan,
+                                        int64_t* nnz_out, int64_t* bad, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    check_shape(n_rows, n_cols);
+    if (index_width != 4 && index_width != 8) fail(SPMVB_INVALID_ARG, "index_width must be 4 or 8");
+    if (nnz_in < 0) fail(SPMVB_INVALID_ARG, "negative nnz");
+    if (nnz_in > INT32_MAX) fail(SPMVB_INVALID_ARG, "nnz %lld exceeds the int32 row-pointer range", (long long)nnz_in);
+    auto* p = new spmvb_canon();
+    p->n_in = nnz_in; p->n_rows = n_rows; p->n_cols = n_cols; p->index_width = index_width;
+    p->row = row; p->col = col; p->val = val;
+    p->colbits = bits_for(n_cols > 0 ? static_cast<uint64_t>(n_cols - 1) : 0);
+    const int rowbits = bits_for(n_rows > 0 ? static_cast<uint64_t>(n_rows - 1) : 0);
+    try {
+      if (nnz_in == 0) {
+        p->fast = true;
+        p->n_out = 0;
+      } else {
+        p->keys_a = DevBuf<uint64_t>(nnz_in, s);
+        DevBuf<unsigned long long> d_bad(1, s);
+        DevBuf<int> d_flag(1, s);
+        unsigned long long init_bad = ~0ull;
+        int init_flag = 0;
+        SPMVB_CUDA(cudaMemcpyAsync(d_bad.get(), &init_bad, sizeof(init_bad), cudaMemcpyHostToDevice, s));
+        SPMVB_CUDA(cudaMemcpyAsync(d_flag.get(), &init_flag, sizeof(init_flag), cudaMemcpyHostToDevice, s));
+        unsigned g = grid_for(nnz_in, 256, 148 * 16);
+        if (index_width == 4)
+          k_canon_prepare<int32_t><<<g, 256, 0, s>>>(static_cast<const int32_t*>(row), static_cast<const int32_t*>(col),
+                                                     val, nnz_in, n_rows, n_cols, p->colbits, p->keys_a.get(),
+                                                     d_bad.get(), d_flag.get());
+        else
+          k_canon_prepare<int64_t><<<g, 256, 0, s>>>(static_cast<const int64_t*>(row), static_cast<const int64_t*>(col),
+                                                     val, nnz_in, n_rows, n_cols, p->colbits, p->keys_a.get(),
+                                                     d_bad.get(), d_flag.get());
+        SPMVB_LAUNCHED("k_canon_prepare");
+        unsigned long long h_bad = 0;
+        int h_flag = 0;
+        SPMVB_CUDA(cudaMemcpyAsync(&h_bad, d_bad.get(), sizeof(h_bad), cudaMemcpyDeviceToHost, s));
+        SPMVB_CUDA(cudaMemcpyAsync(&h_flag, d_flag.get(), sizeof(h_flag), cudaMemcpyDeviceToHost, s));
+        SPMVB_CUDA(cudaStreamSynchronize(s));
+        if (h_bad != ~0ull) {
+          int64_t br = 0, bc = 0;
+          if (index_width == 4) {
+            int32_t t[2];
+            SPMVB_CUDA(cudaMemcpyAsync(&t[0], static_cast<const int32_t*>(row) + h_bad, 4, cudaMemcpyDeviceToHost, s));
+            SPMVB_CUDA(cudaMemcpyAsync(&t[1], static_cast<const int32_t*>(col) + h_bad, 4, cudaMemcpyDeviceToHost, s));
+            SPMVB_CUDA(cudaStreamSynchronize(s));
+            br = t[0]; bc = t[1];
+          } else {
+            SPMVB_CUDA(cudaMemcpyAsync(&br, static_cast<const int64_t*>(row) + h_bad, 8, cudaMemcpyDeviceToHost, s));
+            SPMVB_CUDA(cudaMemcpyAsync(&bc, static_cast<const int64_t*>(col) + h_bad, 8, cudaMemcpyDeviceToHost, s));
+            SPMVB_CUDA(cudaStreamSynchronize(s));
+          }
+          if (bad) { bad[0] = (int64_t)h_bad; bad[1] = br; bad[2] = bc; }
+          fail(SPMVB_OUT_OF_RANGE, "entry %lld at (%lld, %lld) is outside %lldx%lld", (long long)h_bad,
+               (long long)br, (long long)bc, (long long)n_rows, (long long)n_cols);
+        }
+        if (!h_flag) {
+          p->fast = true;
+          p->n_out = nnz_in;
+          p->keys_a.release();
+        } else {
+          p->keys_b = DevBuf<uint64_t>(nnz_in, s);
+          p->vals_b = DevBuf<uint32_t>(nnz_in, s);
+          p->vals_s = DevBuf<uint32_t>(nnz_in, s);
+          RadixSortResult rs = radix_sort_pairs(p->keys_a.get(), nullptr, p->keys_b.get(), p->vals_b.get(),
+                                                p->vals_s.get(), nnz_in, rowbits + p->colbits, s);
+          p->skeys = rs.keys;
+          p->sidx = rs.vals;
+          p->sums = DevBuf<double>(nnz_in, s);
+          p->keep = DevBuf<uint8_t>(nnz_in, s);
+          p->pos = DevBuf<uint32_t>(nnz_in, s);
+          k_canon_runs<<<grid_for(nnz_in, 256, 148 * 16), 256, 0, s>>>(p->skeys, p->sidx, val, nnz_in,
+                                                                       p->sums.get(), p->keep.get());
+          SPMVB_LAUNCHED("k_canon_runs");
+          DevBuf<uint32_t> d_total(1, s);
+          const uint8_t* kp = p->keep.get();
+          uint32_t* pp = p->pos.get();
+          exclusive_scan<uint32_t>(
+              nnz_in, [=] __device__(int64_t i) { return static_cast<uint32_t>(kp[i]); },
+              ArrayStore<uint32_t>{pp}, OpSum{}, 0u, d_total.get(), s);
+          uint32_t h_total = 0;
+          SPMVB_CUDA(cudaMemcpyAsync(&h_total, d_total.get(), sizeof(h_total), cudaMemcpyDeviceToHost, s));
+          SPMVB_CUDA(cudaStreamSynchronize(s));
+          p->n_out = h_total;
+          // Buffers not holding the sorted keys/indices are no longer needed.
+          if (p->skeys != p->keys_a.get()) p->keys_a.release(); else p->keys_b.release();
+          if (p->sidx != p->vals_b.get()) p->vals_b.release(); else p->vals_s.release();
+        }
+      }
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *plan = p;
+    *nnz_out = p->n_out;
+  });
+}
+
+extern "C" int spmvb_canonicalize_finish(spmvb_canon* p, int32_t* row_out, int32_t* col_out, double* val_out,
+                                         void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (!p) fail(SPMVB_INVALID_ARG, "null plan");
+    if (p->n_out > 0) {
+      unsigned g = grid_for(p->n_in, 256, 148 * 16);
+      if (p->fast) {
+        if (p->index_width == 4)
+          k_narrow_copy<int32_t><<<g, 256, 0, s>>>(static_cast<const int32_t*>(p->row),
+                                                   static_cast<const int32_t*>(p->col), p->val, p->n_in, row_out,
+                                                   col_out, val_out);
+        else
+          k_narrow_copy<int64_t><<<g, 256, 0, s>>>(static_cast<const int64_t*>(p->row),
+                                                   static_cast<const int64_t*>(p->col), p->val, p->n_in, row_out,
+                                                   col_out, val_out);
+        SPMVB_LAUNCHED("k_narrow_copy");
+      } else {
+        k_canon_emit<<<g, 256, 0, s>>>(p->skeys, p->sums.get(), p->keep.get(), p->pos.get(), p->n_in, p->colbits,
+                                       row_out, col_out, val_out);
+        SPMVB_LAUNCHED("k_canon_emit");
+      }
+    }
+    delete p;
+  });
+}
+
+extern "C" void spmvb_canonicalize_free(spmvb_canon* p) { delete p; }
+
+namespace spmvb {
+// ptr[0..n_rows] from row-sorted COO rows (histogram + exclusive scan).
+void build_row_ptr(const int32_t* row, int64_t nnz, int64_t n_rows, int32_t* ptr, cudaStream_t s) {
+  DevBuf<unsigned int> counts(n_rows > 0 ? n_rows : 1, s);
+  if (n_rows > 0) SPMVB_CUDA(cudaMemsetAsync(counts.get(), 0, n_rows * sizeof(unsigned int), s));
+  if (nnz > 0) {
+    k_row_counts<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(row, nnz, counts.get());
+    SPMVB_LAUNCHED("k_row_counts");
+  }
+  const unsigned int* c = counts.get();
+  const int64_t n = n_rows;
+  exclusive_scan<int32_t>(
+      n_rows + 1, [=] __device__(int64_t i) { return i < n ? static_cast<int32_t>(c[i]) : 0; },
+      ArrayStore<int32_t>{ptr}, OpSum{}, 0, static_cast<int32_t*>(nullptr), s);
+}
+}  // namespace spmvb
+
+extern "C" int spmvb_row_nnz_histogram(const int32_t* row, int64_t nnz, int64_t n_rows, int64_t* counts_out,
+                                       void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n_rows <= 0) return;
+    DevBuf<unsigned int> counts(n_rows, s);
+    SPMVB_CUDA(cudaMemsetAsync(counts.get(), 0, n_rows * sizeof(unsigned int), s));
+    if (nnz > 0) {
+      k_row_counts<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(row, nnz, counts.get());
+      SPMVB_LAUNCHED("k_row_counts");
+    }
+    k_counts_to_i64<<<grid_for(n_rows, 256, 148 * 16), 256, 0, s>>>(counts.get(), n_rows, counts_out);
+    SPMVB_LAUNCHED("k_counts_to_i64");
+  });
+}
+
+extern "C" int spmvb_coo_to_csr(const int32_t* row, const int32_t* col, const double* val, int64_t nnz,
+                                int64_t n_rows, int32_t* ptr_out, int32_t* col_out, double* val_out,
+                                void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (nnz > INT32_MAX) fail(SPMVB_INVALID_ARG, "nnz exceeds the int32 row-pointer range");
+    build_row_ptr(row, nnz, n_rows, ptr_out, s);
+    if (nnz > 0) {
+      SPMVB_CUDA(cudaMemcpyAsync(col_out, col, nnz * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      SPMVB_CUDA(cudaMemcpyAsync(val_out, val, nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+  });
+}
+
+extern "C" int spmvb_csr_row_stats(const int32_t* ptr, int64_t n_rows, int64_t* out3, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n_rows <= 0) {
+      out3[0] = out3[1] = out3[2] = 0;
+      return;
+    }
+    DevBuf<int64_t> d(3, s);
+    int64_t* dp = d.get();
+    auto cnt = [=] __device__(int64_t i) { return static_cast<int64_t>(ptr[i + 1] - ptr[i]); };
+    device_reduce<int64_t>(n_rows, cnt, OpMin{}, INT64_MAX, dp + 0, s);
+    device_reduce<int64_t>(n_rows, cnt, OpMax{}, (int64_t)0, dp + 1, s);
+    device_reduce<int64_t>(
+        n_rows, [=] __device__(int64_t i) { return static_cast<int64_t>(ptr[i + 1] > ptr[i] ? 1 : 0); }, OpSum{},
+        (int64_t)0, dp + 2, s);
+    copy_to_host(out3, dp, 3, s);
+  });
+}
+
+extern "C" int spmvb_csr_nonempty_rows(const int32_t* ptr, int64_t n_rows, int32_t* rows_out, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n_rows <= 0) return;
+    exclusive_scan<int32_t>(
+        n_rows, [=] __device__(int64_t i) { return ptr[i + 1] > ptr[i] ? 1 : 0; },
+        [=] __device__(int64_t i, int32_t v) {
+          if (ptr[i + 1] > ptr[i]) rows_out[v] = static_cast<int32_t>(i);
+        },
+        OpSum{}, 0, static_cast<int32_t*>(nullptr), s);
+  });
+}
+
+extern "C" int spmvb_spmv_sequential(int64_t n_rows, const int32_t* ptr, const int32_t* col, const double* val,
+                                     const double* x, double* y, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n_rows <= 0) return;
+    k_spmv_sequential<<<grid_for(n_rows, 128, 148 * 64), 128, 0, s>>>(n_rows, ptr, col, val, x, y);
+    SPMVB_LAUNCHED("k_spmv_sequential");
+  });
+}
+
+extern "C" int spmvb_sumsq(const double* y, int64_t n, double* out, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    device_reduce<double>(
+        n, [=] __device__(int64_t i) { double v = y[i]; return v * v; }, OpSum{}, 0.0, out, s);
+  });
+}
+
+extern "C" int spmvb_inv_sqrt(const double* sumsq, double* scale_out, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    k_inv_sqrt<<<1, 1, 0, s>>>(sumsq, scale_out);
+    SPMVB_LAUNCHED("k_inv_sqrt");
+  });
+}

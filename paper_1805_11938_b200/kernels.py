@@ -1,0 +1,177 @@
+"""SpMV entry points, one per storage format, plus the tag dispatcher.
+
+Mirrors spmvkit.kernels (/root/reference/pkg/src/spmvkit/kernels.py): the
+same names, signatures (``workers`` is accepted for compatibility; the GPU
+kernel fixes its own decomposition) and error behaviour
+(``ValueError("x has length L, expected N")``, ``ValueError("... does not
+match ...")``).  Every call launches hand-written sm_100a kernels through
+libspmvb.so; there is no CPU fallback.
+
+Containers: a float64 CUDA tensor ``x`` gives a CUDA tensor ``y`` (no host
+traffic); a CPU tensor gives a CPU tensor (pinned in -> pinned out, copies
+on the current stream); anything else (numpy, list) is coerced like the
+reference (``np.asarray(x, float64).ravel()``) and returns a numpy array.
+Keyword-only extensions: ``out=`` (device output buffer) and ``scale=`` (a
+device scalar multiplying every row result; power iteration uses it).
+Repeated calls are bit-identical (no floating-point atomics).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import LIB, check, ptr
+from .formats import Csr5Matrix, CsrMatrix, EllMatrix, FormatMatrix, FormatTag, HybMatrix, SellMatrix
+
+__all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_ell", "spmv_hyb", "spmv_sell"]
+
+
+def plan_row_blocks(n_rows: int, workers: int) -> list[tuple[int, int]]:
+    """Host task plan of the reference CPU path (kernels.py:61-66); kept for
+    API compatibility.  The GPU kernels decompose by merge-path tiles,
+    CSR5 tiles or rows instead."""
+    if n_rows == 0:
+        return []
+    block = max(1, n_rows // (4 * max(workers, 1)))
+    return [(lo, min(lo + block, n_rows)) for lo in range(0, n_rows, block)]
+
+
+def _prepare_x(x, n_cols: int, device: torch.device):
+    """Move/validate x; returns (device tensor, how to return y)."""
+    if isinstance(x, torch.Tensor):
+        xv = x.reshape(-1)
+        if xv.shape[0] != n_cols:
+            raise ValueError(f"x has length {xv.shape[0]}, expected {n_cols}")
+        if xv.is_cuda:
+            if xv.device != device:
+                raise ValueError(f"x is on {xv.device}, matrix is on {device}")
+            return xv.to(torch.float64).contiguous(), ("cuda",)
+        pinned = xv.is_pinned()
+        xd = xv.to(torch.float64).contiguous().to(device, non_blocking=pinned)
+        return xd, ("cpu", pinned)
+    arr = np.asarray(x, dtype=np.float64).ravel()
+    if arr.shape[0] != n_cols:
+        raise ValueError(f"x has length {arr.shape[0]}, expected {n_cols}")
+    xd = torch.from_numpy(np.ascontiguousarray(arr)).to(device)
+    return xd, ("numpy",)
+
+
+def _finish_y(y: torch.Tensor, how):
+    if how[0] == "cuda":
+        return y
+    if how[0] == "cpu":
+        pinned = how[1]
+        host = torch.empty(y.shape, dtype=y.dtype, pin_memory=pinned)
+        host.copy_(y, non_blocking=pinned)
+        if pinned:
+            torch.cuda.current_stream(y.device).synchronize()
+        return host
+    return y.cpu().numpy()
+
+
+def _out(m, out):
+    if out is None:
+        return torch.empty(m.n_rows, dtype=torch.float64, device=m.device)
+    if out.dtype != torch.float64 or not out.is_cuda or out.numel() != m.n_rows or not out.is_contiguous():
+        raise ValueError("out must be a contiguous float64 CUDA tensor with n_rows elements")
+    return out
+
+
+def _run(m, x, out, scale, launch):
+    xd, how = _prepare_x(x, m.n_cols, m.device)
+    y = _out(m, out)
+    if m.n_rows:
+        with torch.cuda.device(m.device):
+            launch(xd, y, ptr(scale) if scale is not None else None, _lib.stream(m.device))
+    return _finish_y(y, how)
+
+
+def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None):
+    """y = A x for CSR via the merge-path kernel (kernels.py:76-95)."""
+    plan = m.merge_plan()
+
+    def launch(xd, y, sp, s):
+        cr, cv = plan.scratch(m.device)
+        check(
+            LIB.spmvb_spmv_csr(
+                m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.tile_row), ptr(plan.tile_nz),
+                ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
+            )
+        )
+
+    return _run(m, x, out, scale, launch)
+
+
+def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None):
+    """y = A x for CSR5: per-tile segmented sums + ordered carry fix-up (kernels.py:139-174)."""
+
+    def launch(xd, y, sp, s):
+        carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
+        check(
+            LIB.spmvb_spmv_csr5(
+                m.n_rows, m.nnz, m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag), ptr(m.indices), ptr(m.data),
+                ptr(m.tile_aux), ptr(m.nonempty_rows), m.n_nonempty, ptr(carry), ptr(xd), ptr(y), sp, s,
+            )
+        )
+
+    return _run(m, x, out, scale, launch)
+
+
+def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
+    """y = A x for ELL, sequential over the k slots (kernels.py:98-116)."""
+
+    def launch(xd, y, sp, s):
+        check(LIB.spmvb_spmv_ell(m.n_rows, m.k, ptr(m.grid_indices), ptr(m.grid_data), ptr(xd), ptr(y), sp, s))
+
+    return _run(m, x, out, scale, launch)
+
+
+def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
+    """y = A x for SELL / SELL-C-sigma, scattered through perm (kernels.py:119-136)."""
+
+    def launch(xd, y, sp, s):
+        perm = m.perm if m.sigma > 0 else None
+        check(
+            LIB.spmvb_spmv_sell(
+                m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
+                ptr(xd), ptr(y), sp, s,
+            )
+        )
+
+    return _run(m, x, out, scale, launch)
+
+
+def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None):
+    """y = ELL part + COO tail (kernels.py:177-199), one fused kernel."""
+    plan = m.merge_plan()
+
+    def launch(xd, y, sp, s):
+        cr, cv = plan.scratch(m.device)
+        t = m.coo_tail
+        check(
+            LIB.spmvb_spmv_hyb(
+                m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), t.nnz, ptr(m.tail_ptr), ptr(t.col),
+                ptr(t.data), ptr(plan.tile_row), ptr(plan.tile_nz), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
+            )
+        )
+
+    return _run(m, x, out, scale, launch)
+
+
+_KERNELS = {
+    FormatTag.CSR: (CsrMatrix, spmv_csr),
+    FormatTag.CSR5: (Csr5Matrix, spmv_csr5),
+    FormatTag.ELL: (EllMatrix, spmv_ell),
+    FormatTag.SELL: (SellMatrix, spmv_sell),
+    FormatTag.HYB: (HybMatrix, spmv_hyb),
+}
+
+
+def spmv(tag: FormatTag, m: FormatMatrix, x, workers: int = 1, **kw):
+    """Dispatch to the kernel matching ``tag``; the instance type must agree."""
+    cls, kernel = _KERNELS[FormatTag(tag)]
+    if not isinstance(m, cls):
+        raise ValueError(f"format tag {FormatTag(tag).value!r} does not match {type(m).__name__}")
+    return kernel(m, x, workers, **kw)

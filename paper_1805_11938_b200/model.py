@@ -1,0 +1,149 @@
+"""Format selection at deployment time (mirrors the deployment half of
+spmvkit.model: ``predict``, ``select_format``, ``load_model``).
+
+Reference: /root/reference/pkg/src/spmvkit/model.py:216-223 (predict),
+:305-319 (select_format), :322-430 (model text format).  Tree training and
+cross-validation are offline CPU code and out of scope;
+models trained by the reference load here unchanged, and reference
+``DecisionTreeModel`` objects are accepted directly (duck-typed).
+
+``select_format`` = GPU feature extraction (8 scalars come back to the host),
+host tree descent, GPU conversion.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .features import FEATURE_NAMES, FeatureVector, ScalingParams, apply_scaling, extract_features
+from .formats import FormatMatrix, FormatTag, convert
+
+__all__ = ["DecisionTreeModel", "ModelIOError", "TreeNode", "load_model", "predict", "select_format"]
+
+N_FEATURES = len(FEATURE_NAMES)
+N_CLASSES = len(FormatTag)
+
+
+class ModelIOError(ValueError):
+    """A model file could not be parsed or fails structural validation."""
+
+
+@dataclass
+class TreeNode:
+    """Internal node (feature >= 0) or leaf (feature == -1)."""
+
+    feature: int = -1
+    threshold: float = 0.0
+    left: int = -1
+    right: int = -1
+    label: FormatTag | None = None
+    counts: tuple[int, ...] = ()
+
+    @property
+    def is_leaf(self) -> bool:
+        return self.feature < 0
+
+
+@dataclass
+class DecisionTreeModel:
+    nodes: list[TreeNode]
+    max_depth: int
+    min_samples_leaf: int
+    scaling: ScalingParams
+
+
+def predict(model, f: FeatureVector) -> FormatTag:
+    """Scale (clamped) and descend the tree (model.py:216-223)."""
+    vec = apply_scaling(f, model.scaling)
+    node = model.nodes[0]
+    while not node.is_leaf:
+        node = model.nodes[node.left if vec[node.feature] <= node.threshold else node.right]
+    return FormatTag(node.label.value if hasattr(node.label, "value") else node.label)
+
+
+def select_format(
+    a,
+    model,
+    *,
+    omega: int = 4,
+    sigma: int = 16,
+    sell_c: int = 4,
+    sell_sigma: int = 0,
+) -> tuple[FormatTag, FormatMatrix]:
+    """Extract features, predict the format, convert (model.py:305-319)."""
+    tag = predict(model, extract_features(a))
+    return tag, convert(tag, a, omega=omega, sigma=sigma, sell_c=sell_c, sell_sigma=sell_sigma)
+
+
+def _parse_line(toks: list[str], nodes: dict, mins: np.ndarray, maxs: np.ndarray) -> None:
+    kind = toks[0]
+    if kind == "node" and len(toks) == 7 and toks[2] == "split":
+        nodes[int(toks[1])] = TreeNode(feature=int(toks[3]), threshold=float(toks[4]), left=int(toks[5]),
+                                       right=int(toks[6]))
+    elif kind == "leaf" and len(toks) == 3 + N_CLASSES:
+        nodes[int(toks[1])] = TreeNode(label=FormatTag(toks[2]), counts=tuple(int(c) for c in toks[3:]))
+    elif kind == "scale" and len(toks) == 4:
+        f = int(toks[1])
+        if not 0 <= f < N_FEATURES:
+            raise ValueError(f"feature index {f}")
+        mins[f] = float(toks[2])
+        maxs[f] = float(toks[3])
+    else:
+        raise ValueError("unrecognized line")
+
+
+def _ordered_tree(nodes: dict[int, TreeNode]) -> list[TreeNode]:
+    if 0 not in nodes:
+        raise ModelIOError("model has no root node 0")
+    missing = [i for i in range(len(nodes)) if i not in nodes]
+    if missing:
+        raise ModelIOError(f"node ids are not contiguous: missing {missing[0]}")
+    tree = [nodes[i] for i in range(len(nodes))]
+    visited: set[int] = set()
+    todo = [0]
+    while todo:
+        i = todo.pop()
+        if i in visited:
+            raise ModelIOError(f"node {i} is reachable twice")
+        visited.add(i)
+        if not tree[i].is_leaf:
+            for child in (tree[i].left, tree[i].right):
+                if not 0 <= child < len(tree):
+                    raise ModelIOError(f"node {i} points at missing child {child}")
+                todo.append(child)
+    if len(visited) != len(tree):
+        raise ModelIOError("model contains unreachable nodes")
+    return tree
+
+
+def load_model(source) -> DecisionTreeModel:
+    """Read the reference's ``spmvkit-model v1`` text format (model.py:322-430)."""
+    text = source.read() if hasattr(source, "read") else Path(source).read_text()
+    lines = [ln for ln in text.splitlines() if ln.strip()]
+    if not lines:
+        raise ModelIOError("empty model file")
+    head = lines[0].split()
+    ok = len(head) == 6 and head[:3] == ["spmvkit-model", "v1", "max_depth"] and head[4] == "min_samples_leaf"
+    try:
+        if not ok:
+            raise ValueError
+        max_depth, min_leaf = int(head[3]), int(head[5])
+    except ValueError:
+        raise ModelIOError(f"bad model header {lines[0]!r}") from None
+    nodes: dict[int, TreeNode] = {}
+    mins = np.full(N_FEATURES, np.nan)
+    maxs = np.full(N_FEATURES, np.nan)
+    for line in lines[1:]:
+        try:
+            _parse_line(line.split(), nodes, mins, maxs)
+        except ValueError as exc:
+            raise ModelIOError(f"bad model line {line!r}: {exc}") from None
+    if np.isnan(mins).any() or np.isnan(maxs).any():
+        raise ModelIOError("model file is missing scale lines")
+    for node in nodes.values():
+        if not node.is_leaf and not 0 <= node.feature < N_FEATURES:
+            raise ModelIOError(f"split on unknown feature {node.feature}")
+    return DecisionTreeModel(_ordered_tree(nodes), max_depth, min_leaf, ScalingParams(mins, maxs))

@@ -1,0 +1,215 @@
+"""GPU parity against the reference's fixtures (tests/golden/cases.npz) and
+the CPU oracle.  Every call goes through the C ABI (libspmvb.so).
+
+Bar: conversions and canonicalize bit-exact (indices by value, fp64 by
+bits); ELL/SELL SpMV and dense_spmv_oracle bit-identical to the reference;
+CSR/CSR5/HYB SpMV within |y - y_ref| <= 1e-12 * (|A| |x|) elementwise (the
+north-star tolerance) and <= 1e-12 * (1 + |y_ref|) (the reference tests'
+tolerance, test_kernels.py:25-30); repeated runs bit-identical.
+"""
+
+from __future__ import annotations
+
+import io
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import demo_triplets, random_triplets
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+CSR5_PARAMS = [(2, 2), (4, 16), (32, 16), (3, 5), (4, 3), (1, 1), (8, 4), (16, 2)]
+SELL_PARAMS = [(4, 0), (2, 4), (3, 0), (4, 8), (32, 64), (1, 0), (2, 2)]
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def sp():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1805_11938_b200 as sp
+
+    return sp
+
+
+def np_(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def same_bits(a, b) -> bool:
+    a, b = np.asarray(np_(a), dtype=np.float64), np.asarray(np_(b), dtype=np.float64)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def assert_within(y, ref, absA_absx):
+    y, ref = np_(y), np.asarray(ref)
+    d = np.abs(y - ref)
+    assert np.all(d <= TOL * absA_absx), float((d - TOL * absA_absx).max())
+    assert np.all(d <= TOL * (1.0 + np.abs(ref)))
+
+
+def abs_bound(g, nr):
+    return port.dense_spmv_oracle(g["row"], g["col"], np.abs(g["data"]), nr, np.abs(g["x"]))
+
+
+def test_every_case_matches_reference(sp, golden):
+    for name in golden.names:
+        g = golden.case(name)
+        nr, nc = (int(t) for t in g["shape"])
+        a = sp.canonicalize(g["in_row"], g["in_col"], g["in_val"], nr, nc)
+        assert np.array_equal(np_(a.row), g["row"]) and np.array_equal(np_(a.col), g["col"]), name
+        assert same_bits(a.data, g["data"]), name
+        assert np.array_equal(np_(sp.row_nnz_histogram(a)), g["counts"]), name
+        x = torch.from_numpy(g["x"]).cuda()
+        bound = abs_bound(g, nr)
+        assert same_bits(sp.dense_spmv_oracle(a, x), g["y_oracle"]), name
+        m = sp.to_csr(a)
+        assert np.array_equal(np_(m.ptr), g["csr/ptr"]), name
+        y = sp.spmv("csr", m, x)
+        assert_within(y, g["y_oracle"], bound)
+        assert same_bits(sp.spmv("csr", m, x), y)
+        for om, sg in CSR5_PARAMS:
+            q = f"csr5_{om}_{sg}/"
+            m5 = sp.to_csr5(a, om, sg)
+            for f in ("tile_ptr", "bit_flag", "y_off", "seg_off", "indices"):
+                assert np.array_equal(np_(getattr(m5, f)), g[q + f]), (name, q, f)
+            assert same_bits(m5.data, g[q + "data"]), (name, q)
+            y5 = sp.spmv("csr5", m5, x)
+            assert_within(y5, g["y_oracle"], bound)
+            assert same_bits(sp.spmv("csr5", m5, x), y5)
+            assert sp.coo_equal(sp.to_coo(m5), a), (name, q)
+        if int(g["ell/k"]) >= 0:
+            me = sp.to_ell(a)
+            assert me.k == int(g["ell/k"]), name
+            assert np.array_equal(np_(me.indices), g["ell/indices"]), name
+            assert same_bits(me.data.contiguous(), g["ell/data"]) and np.array_equal(np_(me.row_nnz), g["ell/row_nnz"])
+            assert same_bits(sp.spmv("ell", me, x), g["ell/y"]), name
+            assert sp.coo_equal(sp.to_coo(me), a), name
+        for cc, ss in SELL_PARAMS:
+            q = f"sell_{cc}_{ss}/"
+            ms = sp.to_sell(a, cc, ss)
+            assert np.array_equal(np_(ms.perm), g[q + "perm"]), (name, q)
+            assert np.array_equal(np_(ms.widths), g[q + "widths"]), (name, q)
+            assert np.array_equal(np_(ms.row_nnz_perm), g[q + "row_nnz_perm"]), (name, q)
+            assert np.array_equal(np_(ms.flat_indices), g[q + "flat_indices"]), (name, q)
+            assert same_bits(ms.flat_data, g[q + "flat_data"]), (name, q)
+            assert same_bits(sp.spmv("sell", ms, x), g[q + "y"]), (name, q)
+            assert sp.coo_equal(sp.to_coo(ms), a), (name, q)
+        mh = sp.to_hyb(a)
+        assert mh.k == int(g["hyb/k"]), name
+        assert np.array_equal(np_(mh.ell.indices), g["hyb/ell_indices"]), name
+        assert same_bits(mh.ell.data.contiguous(), g["hyb/ell_data"]), name
+        assert np.array_equal(np_(mh.ell.row_nnz), g["hyb/ell_row_nnz"]), name
+        assert np.array_equal(np_(mh.coo_tail.row), g["hyb/tail_row"]), name
+        assert np.array_equal(np_(mh.coo_tail.col), g["hyb/tail_col"]), name
+        assert same_bits(mh.coo_tail.data, g["hyb/tail_data"]), name
+        yh = sp.spmv("hyb", mh, x)
+        assert_within(yh, g["y_oracle"], bound)
+        assert sp.coo_equal(sp.to_coo(mh), a), name
+        assert sp.coo_equal(sp.to_coo(m), a), name
+        if nr and nc:
+            f = sp.extract_features(a)
+            assert f.as_array().tobytes() == g["features"].tobytes(), name
+        if nr:
+            assert sp.hyb_typical_k(g["counts"]) == int(g["hyb_k"]), name
+        got = [sp.bandwidth_estimate("csr", m, 1.0), sp.bandwidth_estimate("csr5", sp.to_csr5(a, 4, 16), 1.0),
+               sp.bandwidth_estimate("sell", sp.to_sell(a, 4, 0), 1.0), sp.bandwidth_estimate("hyb", mh, 1.0)]
+        assert got == g["bytes"].tolist(), name
+
+
+def test_demo_hand_results(sp):
+    r, c, v = demo_triplets()
+    a = sp.canonicalize(r, c, v, 4, 4)
+    for tag in sp.FormatTag:
+        m = sp.convert(tag, a, omega=2, sigma=2, sell_c=2, sell_sigma=4)
+        assert sp.spmv(tag, m, np.ones(4)).tolist() == [7.0, 13.0, 4.0, 12.0]
+        assert sp.spmv(tag, m, np.zeros(4)).tolist() == [0.0] * 4
+        with pytest.raises(ValueError, match="length"):
+            sp.spmv(tag, m, np.ones(5))
+    with pytest.raises(ValueError, match="does not match"):
+        sp.spmv("hyb", sp.to_csr(a), np.ones(4))
+    f = sp.extract_features(a)
+    assert f.nnz_std == math.sqrt(0.5) and f.variation == math.sqrt(0.5) / 2.0 and f.nnz_frac == 0.5
+
+
+def test_containers(sp):
+    r, c, v = demo_triplets()
+    m = sp.to_csr(sp.canonicalize(r, c, v, 4, 4))
+    y = sp.spmv("csr", m, [1, 1, 1, 1])
+    assert isinstance(y, np.ndarray) and y.tolist() == [7.0, 13.0, 4.0, 12.0]
+    yc = sp.spmv("csr", m, torch.ones(4, dtype=torch.float64).pin_memory())
+    assert isinstance(yc, torch.Tensor) and not yc.is_cuda and yc.tolist() == [7.0, 13.0, 4.0, 12.0]
+    yd = sp.spmv("csr", m, torch.ones(4, dtype=torch.float64, device="cuda"))
+    assert yd.is_cuda
+
+
+def test_errors(sp):
+    r, c, v = demo_triplets()
+    a = sp.canonicalize(r, c, v, 4, 4)
+    with pytest.raises(ValueError, match="omega"):
+        sp.to_csr5(a, 0, 2)
+    with pytest.raises(ValueError, match="sigma"):
+        sp.to_csr5(a, 4, 0)
+    with pytest.raises(ValueError, match="multiple"):
+        sp.to_sell(a, 2, 3)
+    big = sp.canonicalize([0] * 8 + [1], list(range(8)) + [0], [1.0] * 9, 64, 8)
+    with pytest.raises(sp.ConversionError, match="cell"):
+        sp.to_ell(big, max_cells=100)
+    with pytest.raises(sp.ConversionError, match="cell"):
+        sp.to_sell(big, 4, 0, max_cells=100)
+    with pytest.raises(ValueError, match="outside"):
+        sp.canonicalize([0, 2], [0, 0], [1.0, 1.0], 2, 2)
+    with pytest.raises(ValueError, match="outside"):
+        sp.canonicalize([0], [-1], [1.0], 2, 2)
+    with pytest.raises(ValueError, match="32-bit"):
+        sp.canonicalize([], [], [], 2**32, 1)
+    with pytest.raises(ValueError, match="undefined"):
+        sp.extract_features(sp.canonicalize([], [], [], 0, 5))
+    with pytest.raises(ValueError, match="disagree"):
+        sp.canonicalize([0, 1], [0], [1.0], 2, 2)
+    assert sp.canonicalize([0, 0, 0], [0, 1, 1], [1.0, -1.0, 1.0], 1, 2).data.tolist() == [1.0]
+
+
+def test_random_sweep_against_oracle(sp, rng):
+    for trial in range(40):
+        rr, cc, vv, nr, nc = random_triplets(rng, max_dim=300)
+        # shuffle + duplicate some entries to exercise the radix sort and sums
+        dup = rng.integers(0, max(len(rr), 1), size=len(rr) // 4) if len(rr) else np.empty(0, int)
+        rr = np.concatenate([rr, rr[dup]]); cc = np.concatenate([cc, cc[dup]]); vv = np.concatenate([vv, vv[dup]])
+        perm = rng.permutation(len(rr))
+        rr, cc, vv = rr[perm], cc[perm], vv[perm]
+        a = sp.canonicalize(torch.from_numpy(rr).int(), torch.from_numpy(cc).int(), vv, nr, nc)
+        orow, ocol, oval = port.canonicalize(rr, cc, vv, nr, nc)
+        assert np.array_equal(np_(a.row), orow) and np.array_equal(np_(a.col), ocol)
+        assert same_bits(a.data, oval)
+        x = rng.normal(size=nc)
+        ref = port.dense_spmv_oracle(orow, ocol, oval, nr, x)
+        bound = port.dense_spmv_oracle(orow, ocol, np.abs(oval), nr, np.abs(x))
+        om = int(rng.choice([1, 2, 4, 8, 16, 32, 3, 5]))
+        sg = int(rng.integers(1, 40))
+        for tag, kw in [("csr", {}), ("csr5", dict(omega=om, sigma=sg)), ("ell", {}),
+                        ("sell", dict(sell_c=int(rng.integers(1, 40)), sell_sigma=0)), ("hyb", {})]:
+            m = sp.convert(tag, a, **kw)
+            y = sp.spmv(tag, m, x)
+            assert_within(y, ref, bound)
+            assert sp.coo_equal(sp.to_coo(m), a), (trial, tag)
+
+
+def test_matrix_market_round_trip(sp, rng):
+    demo = ("%%MatrixMarket matrix coordinate real general\n% c\n4 4 8\n1 2 6\n1 3 1\n2 1 2\n2 3 8\n2 4 3\n"
+            "3 3 4\n4 2 7\n4 3 5\n")
+    a = sp.read_matrix_market(io.BytesIO(demo.encode()))
+    assert np_(a.row).tolist() == [0, 0, 1, 1, 1, 2, 3, 3]
+    sym = sp.read_matrix_market(b"%%MatrixMarket matrix coordinate real symmetric\n3 3 2\n2 1 5\n3 3 7\n")
+    assert np_(sym.col).tolist() == [1, 0, 2] and np_(sym.data).tolist() == [5, 5, 7]
+    with pytest.raises(sp.MatrixMarketError, match="line 3"):
+        sp.read_matrix_market(b"%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 9\n")
+    rr, cc, vv, nr, nc = random_triplets(rng, max_dim=60)
+    b = sp.canonicalize(rr, cc, vv, nr, nc)
+    buf = io.StringIO()
+    sp.write_matrix_market(b, buf)
+    assert sp.coo_equal(sp.read_matrix_market(buf.getvalue().encode()), b)
