@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 SpMV GFLOP/s (2*nnz/t) and HBM GB/s per format on B200.
+
+Workload (default): BASELINE.json configs[4] "C5" — R-MAT scale 25
+(n = 33,554,432), edge factor 16 (~5.3e8 nnz after first-draw dedup),
+(a,b,c,d) = (0.57,0.19,0.19,0.05), values U(0,1], x ~ U[-1,1];
+nnz-balanced 1-D row-block partition over N GPUs, power iteration with an
+all-gatherv of x and an all-reduce of ||y||^2 per step.
+One step = one power-iteration step over the whole matrix.  The matrix
+(~7 GB) is larger than L2, so no flush is needed between steps.
+
+Our arm:   python bench.py [--gpus N --steps K --warmup W]
+Reference: python bench.py --impl reference  (the reference's CPU algorithm,
+           oracle/port.py restating spmvkit.kernels.spmv_csr, on all host
+           cores, on a bounded row sample of the same matrix)
+
+Prints one JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "fp64 SpMV GFLOP/s (2*nnz/t), power-iteration step incl. all-gather of x"
+WORKLOADS = {
+    "C5": dict(scale=25, edge_factor=16, seed=105, x_seed=205),
+    "C4": dict(scale=21, edge_factor=10, seed=104, x_seed=204),
+}
+# GPU-tuned parameters for the per-format candidates;
+# max_cells is raised explicitly above the reference default 2^26 so that
+# SELL can be measured on R-MAT (ELL still cannot: k*n is ~1e13 cells).
+CANDIDATES = [
+    ("csr", {}),
+    ("csr5", dict(omega=32, sigma=16)),
+    ("hyb", dict(max_cells=1 << 34)),
+    ("sell", dict(sell_c=32, sell_sigma=32 * 256, max_cells=1 << 34)),
+    ("ell", dict(max_cells=1 << 34)),
+]
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling in the background."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int, interval_ms: int = 50):
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.t0 = time.time()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu=timestamp,{self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(device_index), "-lms", str(interval_ms)],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        self.proc.wait()
+        self.file.flush()
+        rows = []
+        for line in Path(self.file.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 10:
+                rows.append(parts)
+        os.unlink(self.file.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[6 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+# --------------------------------------------------------------------------
+# Reference arm: the reference's CPU algorithm on a bounded sample
+# --------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import cpu_baseline, port, synth_ref
+
+    w = WORKLOADS[args.workload]
+    cores = port.host_cores()
+    ptr, ind, dat, n_s, n = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"], args.cpu_keep_mod,
+                                                         cores)
+    x = synth_ref.uniform(n, w["x_seed"])
+    nnz_s = int(ind.size)
+    for _ in range(max(args.warmup, 1)):
+        port.spmv_csr(ptr, ind, dat, n_s, x, cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        port.spmv_csr(ptr, ind, dat, n_s, x, cores)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    gflops = 2.0 * nnz_s / t / 1e9
+    sample = (f"rows with mix64(r^0xA5A5A5A5) % {args.cpu_keep_mod} == 0 of {args.workload}: {n_s} rows, "
+              f"{nnz_s} nnz, full-length x ({n}); spmvkit.kernels.spmv_csr algorithm (oracle/port.py), "
+              f"workers={cores}")
+    emit({
+        "impl": "reference", "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "format": "csr", "n": n, "sample_nnz": nnz_s,
+                   "parallelism": f"cpu threads x{cores}"},
+        "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu": cpu_baseline.cpu_model()},
+        "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
+
+
+# --------------------------------------------------------------------------
+# Our arm
+# --------------------------------------------------------------------------
+def event_time(fn, reps: int, warm: int = 3) -> float:
+    """Average seconds per call of fn() timed with CUDA events on the current stream."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / 1e3 / reps
+
+
+def run_ours(args):
+    import torch.distributed as dist
+
+    import paper_1805_11938_b200 as sp
+    from paper_1805_11938_b200 import _lib, dist as spdist, synth
+    from paper_1805_11938_b200.harness import spmv_bytes
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = WORKLOADS[args.workload]
+    warmup = max(args.warmup, 3)
+
+    # ---- build the matrix (untimed setup; conversion times are reported) ----
+    t0 = time.perf_counter()
+    r, c, v = synth.rmat_triplets(w["scale"], w["edge_factor"], w["seed"], dev)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    n = 1 << w["scale"]
+    t0 = time.perf_counter()
+    a = sp.canonicalize(r, c, v, n, n)
+    torch.cuda.synchronize()
+    t_canon = time.perf_counter() - t0
+    raw_nnz = int(r.numel())
+    del r, c, v
+    t0 = time.perf_counter()
+    csr_full = sp.to_csr(a)
+    torch.cuda.synchronize()
+    t_csr = time.perf_counter() - t0
+    nnz = csr_full.nnz
+    del a
+    bounds = spdist.nnz_balanced_bounds(csr_full.ptr, world)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    shard = spdist.row_block(csr_full, lo, hi) if world > 1 else csr_full
+    if world > 1:
+        del csr_full
+    x_full = synth.uniform_vector(n, w["x_seed"], device=dev)
+    torch.cuda.empty_cache()
+
+    # ---- per-format candidates on this shard ----
+    formats = {}
+    best = None
+    wanted = [f.strip() for f in args.formats.split(",") if f.strip()]
+    y_tmp = torch.empty(shard.n_rows, dtype=torch.float64, device=dev)
+    for tag, kw in CANDIDATES:
+        if tag not in wanted:
+            continue
+        rec = {"params": {k: v for k, v in kw.items() if k != "max_cells"}}
+        try:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m = sp.convert(tag, shard, **kw)
+            if tag in ("csr", "hyb"):
+                m.merge_plan()
+            torch.cuda.synchronize()
+            rec["convert_ms"] = (time.perf_counter() - t0) * 1e3
+        except (sp.ConversionError, MemoryError, RuntimeError) as exc:
+            rec["error"] = f"{type(exc).__name__}: {str(exc)[:120]}"
+            formats[tag] = rec
+            torch.cuda.empty_cache()
+            continue
+        t = event_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), reps=args.kernel_reps)
+        b = spmv_bytes(tag, m)
+        rec.update(ms=t * 1e3, gflops=2.0 * m.nnz / t / 1e9, gbs_model=b / t / 1e9, bytes_model=b)
+        formats[tag] = rec
+        if best is None or t < best[2]:
+            if best is not None:
+                del best
+            best = (tag, m, t)
+        else:
+            del m
+        torch.cuda.empty_cache()
+    if best is None:
+        raise RuntimeError("no format converted")
+    tag, m, t_kernel = best
+    # all ranks must agree on one format: take rank 0's choice
+    if world > 1:
+        choice = torch.tensor([[c for c, _ in CANDIDATES].index(tag)], device=dev)
+        dist.broadcast(choice, 0)
+        want = [c for c, _ in CANDIDATES][int(choice.item())]
+        if want != tag:
+            tag = want
+            m = sp.convert(tag, shard, **dict(CANDIDATES)[tag])
+            t_kernel = event_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), reps=args.kernel_reps)
+
+    # ---- roofline of the dominant kernel (this rank's shard) ----
+    peak, peak_src = measured_peak()
+    bytes_model = spmv_bytes(tag, m)
+    achieved = bytes_model / t_kernel / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{args.workload}/{tag}/n{world}")
+        except ValueError:
+            traffic = None
+
+    # ---- timed power iteration ----
+    def local_spmv(xv, out, scale):
+        sp.spmv(tag, m, xv, out=out, scale=scale)
+
+    pi = spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_full)
+    for _ in range(warmup):
+        pi.step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    ramp_end = time.perf_counter() + args.clock_ramp_s
+    ramp_steps = 0
+    while time.perf_counter() < ramp_end:  # keep the GPU busy so clocks are sampled under load
+        pi.step()
+        ramp_steps += 1
+        if ramp_steps % 50 == 0:
+            torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.load().spmvb_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        pi.step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _lib.load().spmvb_launch_count() - launches0
+    clk = clocks.stop()
+    t_loop = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_loop], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_loop = float(tt.item())
+    value = 2.0 * nnz * args.steps / t_loop / 1e9
+
+    # ---- end to end through the public API with host buffers ----
+    x_host = x_full.cpu().pin_memory()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    sp.spmv(tag, m, x_host)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        y_host = sp.spmv(tag, m, x_host)
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = {"value": 2.0 * nnz * e2e_steps / t_e2e / 1e9, "unit": "GFLOP/s",
+           "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(y_host.numel() * 8),
+           "steps": e2e_steps, "api": f"paper_1805_11938_b200.spmv('{tag}', m, pinned_host_x) -> pinned_host_y"}
+
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_baseline, port, synth_ref
+
+        cores = port.host_cores()
+        ptr, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
+                                                             args.cpu_keep_mod, cores)
+        xs = synth_ref.uniform(n, w["x_seed"])
+        tc, reps = cpu_baseline.time_csr(ptr, ind, dat, n_s, xs, cores, min_seconds=args.cpu_seconds)
+        cpu = {"value": 2.0 * ind.size / tc / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+               "sample": (f"{n_s} rows (1/{args.cpu_keep_mod} hashed row sample), {int(ind.size)} nnz, full x; "
+                          f"spmvkit spmv_csr algorithm (oracle/port.py), {reps} reps"),
+               "cpu": cpu_baseline.cpu_model()}
+
+    if rank == 0:
+        emit({
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": warmup, "ms_per_step": t_loop / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "format": tag, "params": formats[tag]["params"], "n": n,
+                       "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
+                       "step": "y=s*A x; ||y||^2 all-reduce; all-gatherv x; s=1/||y||",
+                       "l2": "inputs larger than L2 (matrix >= 6 GB), no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": f"spmv_{tag} (rank 0 shard)", "bytes_per_launch": bytes_model,
+                         "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "formats": formats,
+            "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "to_csr_s": t_csr,
+                           "canonicalize_Mentries_per_s": raw_nnz / t_canon / 1e6},
+        })
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
+    ap.add_argument("--formats", default="csr,csr5,hyb,sell,ell")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--clock-ramp-s", type=float, default=1.0)
+    ap.add_argument("--cpu-keep-mod", type=int, default=64)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -48,6 +48,8 @@ extern "C" {
 
 const char* spmvb_last_error(void);
 int spmvb_abi_version(void);
+/* Number of CUDA kernels this library has launched in the process. */
+unsigned long long spmvb_launch_count(void);
 
 /* ======================================================================== */
 /* COO core — replaces coo.py                                               */

@@ -43,6 +43,7 @@ P_vp = ctypes.POINTER(ctypes.c_void_p)
 SIGNATURES: dict[str, tuple] = {
     "spmvb_last_error": (ctypes.c_char_p, []),
     "spmvb_abi_version": (c_int, []),
+    "spmvb_launch_count": (ctypes.c_ulonglong, []),
     "spmvb_canonicalize_begin": (c_int, [vp, vp, c_int, vp, c_i64, c_i64, c_i64, P_vp, P_i64, P_i64, vp]),
     "spmvb_canonicalize_finish": (c_int, [vp, vp, vp, vp, vp]),
     "spmvb_canonicalize_free": (None, [vp]),

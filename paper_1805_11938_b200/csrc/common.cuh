@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdarg>
@@ -45,8 +46,11 @@ void set_error_message(const char* fmt, ...);
     if (e__ != cudaSuccess) ::spmvb::fail_cuda(e__, #call, __FILE__, __LINE__); \
   } while (0)
 
+extern std::atomic<unsigned long long> g_launches;  // kernels launched by this library
+
 #define SPMVB_LAUNCHED(name)                                        \
   do {                                                              \
+    ::spmvb::g_launches.fetch_add(1, std::memory_order_relaxed);    \
     cudaError_t e__ = cudaGetLastError();                           \
     if (e__ != cudaSuccess) ::spmvb::fail_cuda(e__, name, __FILE__, __LINE__); \
   } while (0)

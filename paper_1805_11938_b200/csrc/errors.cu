@@ -2,6 +2,7 @@
 #include "common.cuh"
 
 namespace spmvb {
+std::atomic<unsigned long long> g_launches{0};
 namespace {
 thread_local std::string g_last_error;
 }
@@ -18,3 +19,4 @@ void set_error_message(const char* fmt, ...) {
 
 extern "C" const char* spmvb_last_error(void) { return spmvb::g_last_error.c_str(); }
 extern "C" int spmvb_abi_version(void) { return SPMVB_ABI_VERSION; }
+extern "C" unsigned long long spmvb_launch_count(void) { return spmvb::g_launches.load(); }

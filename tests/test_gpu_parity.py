@@ -160,7 +160,7 @@ def test_errors(sp):
     with pytest.raises(sp.ConversionError, match="cell"):
         sp.to_ell(big, max_cells=100)
     with pytest.raises(sp.ConversionError, match="cell"):
-        sp.to_sell(big, 4, 0, max_cells=100)
+        sp.to_sell(big, 4, 0, max_cells=10)
     with pytest.raises(ValueError, match="outside"):
         sp.canonicalize([0, 2], [0, 0], [1.0, 1.0], 2, 2)
     with pytest.raises(ValueError, match="outside"):
