@@ -198,6 +198,9 @@ class Sell:
     data: list
     indices: list
     row_nnz_perm: np.ndarray
+    slice_off: np.ndarray
+    flat_indices: np.ndarray
+    flat_data: np.ndarray
 
 
 def to_sell(ptr, indices, data, n_rows, c, sigma=0, max_cells=DEFAULT_MAX_GRID_CELLS):
@@ -223,16 +226,29 @@ def to_sell(ptr, indices, data, n_rows, c, sigma=0, max_cells=DEFAULT_MAX_GRID_C
     total = int((rows_in * widths).sum())
     if total > max_cells:
         raise GridTooLarge(f"sliced grids of {total} cells exceed the {max_cells}-cell limit")
-    # rows gathered into permuted order, then one padded grid, cut per slice
+    # One flat buffer = concatenation of the slices' Fortran-order ravels:
+    # cell (slice s, column j, local row l) at off[s] + j*rows_s + l.
+    off = np.zeros(S + 1, dtype=np.int64)
+    np.cumsum(rows_in * widths, out=off[1:])
+    cell_slice = np.repeat(np.arange(S), rows_in * widths)
+    cell = np.arange(total, dtype=np.int64)
+    cell_row = cell_slice * c + (cell - off[cell_slice]) % np.maximum(rows_in[cell_slice], 1)
+    last = np.zeros(n_rows, dtype=np.int64)  # pad index: last valid column, 0 if empty
+    has = cp > 0
+    last[has] = indices[ptr[perm[has] + 1] - 1]
+    flat_i = last[cell_row] if total else np.empty(0, np.int64)
+    flat_d = np.zeros(total, dtype=np.float64)
     pptr = np.concatenate([[0], np.cumsum(cp)]).astype(np.int64)
-    src = np.repeat(ptr[perm], cp) + (np.arange(int(pptr[-1])) - np.repeat(pptr[:-1], cp))
-    gi_all, gd_all = _grids(n_rows, int(widths.max()) if S else 0, cp, pptr, indices[src], data[src], 1 << 62)
-    ds, ids = [], []
-    for s in range(S):
-        lo, hi, w = s * c, s * c + int(rows_in[s]), int(widths[s])
-        ds.append(np.asfortranarray(gd_all[lo:hi, :w]))
-        ids.append(np.asfortranarray(gi_all[lo:hi, :w]))
-    return Sell(c, sigma, perm, widths, ds, ids, cp)
+    slot = np.arange(int(pptr[-1])) - np.repeat(pptr[:-1], cp)
+    prow = np.repeat(np.arange(n_rows), cp)
+    src = ptr[perm][prow] + slot
+    s_of = prow // c
+    dst = off[s_of] + slot * rows_in[s_of] + (prow - s_of * c)
+    flat_i[dst] = indices[src]
+    flat_d[dst] = data[src]
+    ds = [flat_d[off[s]:off[s + 1]].reshape((int(rows_in[s]), int(widths[s])), order="F") for s in range(S)]
+    ids = [flat_i[off[s]:off[s + 1]].reshape((int(rows_in[s]), int(widths[s])), order="F") for s in range(S)]
+    return Sell(c, sigma, perm, widths, ds, ids, cp, off, flat_i, flat_d)
 
 
 def hyb_typical_k(counts):
@@ -320,15 +336,26 @@ def spmv_sell(m: Sell, n_rows, x, workers=1):
     """kernels.py:119-136."""
     x = np.asarray(x, dtype=np.float64)
     y = np.zeros(n_rows, dtype=np.float64)
-
-    def one(s):
-        d, i = m.data[s], m.indices[s]
-        acc = np.zeros(d.shape[0])
-        for j in range(d.shape[1]):
-            acc += d[:, j] * x[i[:, j]]
-        y[m.perm[s * m.c: s * m.c + d.shape[0]]] = acc
-
-    _map(one, [(s,) for s in range(len(m.data))], workers)
+    if n_rows == 0:
+        return y
+    # Column j of every slice at once: each row still accumulates its slots
+    # in order 0..w-1 (pads included), the reference's per-slice recurrence.
+    S = len(m.data)
+    rows_in = np.minimum(m.c, n_rows - np.arange(S) * m.c)
+    p = np.arange(n_rows)
+    s_of = p // m.c
+    w_of = m.widths[s_of]
+    base = m.slice_off[s_of] + (p - s_of * m.c)
+    stride = rows_in[s_of]
+    acc = np.zeros(n_rows)
+    live = np.nonzero(w_of > 0)[0]
+    j = 0
+    while live.size:
+        o = base[live] + j * stride[live]
+        acc[live] += m.flat_data[o] * x[m.flat_indices[o]]
+        j += 1
+        live = live[w_of[live] > j]
+    y[m.perm] = acc
     return y
 
 

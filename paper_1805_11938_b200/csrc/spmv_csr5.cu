@@ -1,0 +1,432 @@
+// CSR5 SpMV (reference kernels.py:139-174 spmv_csr5): per-tile segmented
+// sums over the reference's descriptor layout, warp shuffles across tile
+// columns, and an ordered carry fix-up for rows spanning tiles.
+#include "spmv_common.cuh"
+
+using namespace spmvb;
+
+namespace {
+
+// =========================================================================
+// CSR5.  Segment ordinal s inside tile t maps to the g-th non-empty row with
+// g = rank(tile_ptr[t]) + s (tile_aux bits 0-30); bit 31 marks a tile whose
+// head continues a row begun earlier: that first segment is a carry.
+// Writing the start segment of non-empty row g also zero-fills the empty
+// rows between non-empty rows g-1 and g (and after the last one).
+// =========================================================================
+struct Csr5Ctx {
+  int64_t n_rows, nnz, n_nonempty;
+  int omega, sigma;
+  const int32_t* tile_ptr;
+  const uint8_t* bit_flag;
+  const int32_t* col;
+  const double* val;
+  const uint32_t* aux;
+  const int32_t* nonempty;
+  double* carry;
+  const double* x;
+  double* y;
+  const double* scale_p;
+};
+
+__device__ __forceinline__ int64_t csr5_row_of(const Csr5Ctx& C, int64_t g) {
+  return C.nonempty ? static_cast<int64_t>(C.nonempty[g]) : g;
+}
+
+__device__ __forceinline__ void csr5_emit(const Csr5Ctx& C, double sc, int64_t t, uint32_t aux, int64_t s, double v) {
+  const bool cont = (aux & 0x80000000u) != 0;
+  if (s == 0 && cont) {
+    C.carry[t] = sc * v;
+    return;
+  }
+  const int64_t g = static_cast<int64_t>(aux & 0x7fffffffu) + s;
+  const int64_t r = csr5_row_of(C, g);
+  C.y[r] = sc * v;
+  if (C.nonempty) {
+    const int64_t prev = g > 0 ? csr5_row_of(C, g - 1) : -1;
+    for (int64_t z = prev + 1; z < r; ++z) C.y[z] = 0.0;
+    if (g == C.n_nonempty - 1)
+      for (int64_t z = r + 1; z < C.n_rows; ++z) C.y[z] = 0.0;
+  }
+}
+
+// Generic: one thread per tile, CSR order recovered from the stored layout.
+__global__ void k_csr5_generic(Csr5Ctx C, int64_t t_begin, int64_t t_end) {
+  const int64_t tile = static_cast<int64_t>(C.omega) * C.sigma;
+  const double sc = load_scale(C.scale_p);
+  for (int64_t t = t_begin + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < t_end;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t base = t * tile;
+    const int64_t m = C.nnz - base < tile ? C.nnz - base : tile;
+    const int64_t q = m / C.sigma, rem = m % C.sigma;
+    const uint32_t aux = C.aux[t];
+    int64_t seg = -1;
+    double sum = 0.0;
+    for (int64_t p = 0; p < m; ++p) {
+      const int64_t gi = p % C.sigma, gj = p / C.sigma;
+      const int64_t pos = base + gi * q + (gi < rem ? gi : rem) + gj;
+      if (C.bit_flag[pos]) {
+        if (seg >= 0) csr5_emit(C, sc, t, aux, seg, sum);
+        ++seg;
+        sum = 0.0;
+      }
+      sum += C.val[pos] * ldx(C.x, C.col[pos]);
+    }
+    if (seg >= 0) csr5_emit(C, sc, t, aux, seg, sum);
+  }
+}
+
+// Fast path: W lanes per full tile (omega == W), lane j owns tile column j
+// (sigma consecutive CSR-order entries stored at base + i*W + j).
+template <int W>
+__global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t full_tiles) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane % W;
+  const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
+  const bool active = group < full_tiles;
+  const int64_t t = active ? group : 0;
+  const int sigma = C.sigma;
+  const int64_t base = t * static_cast<int64_t>(W) * sigma;
+  const uint32_t aux = active ? C.aux[t] : 0u;
+  const double sc = load_scale(C.scale_p);
+
+  double head = 0.0, sum = 0.0;
+  int nflags = 0;
+  // First pass: count this lane's flags so segment ordinals are known while
+  // streaming; flags are 1 byte/entry and re-read from L1.
+  for (int i = 0; i < sigma && active; ++i) nflags += C.bit_flag[base + static_cast<int64_t>(i) * W + j] ? 1 : 0;
+  // Exclusive prefix of flag counts across the group's lanes.
+  int incl = nflags;
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, d, W);
+    if (j >= d) incl += o;
+  }
+  const int seg_base = incl - nflags;
+  int seen = 0;
+  if (active) {
+    for (int i = 0; i < sigma; ++i) {
+      const int64_t pos = base + static_cast<int64_t>(i) * W + j;
+      const bool f = C.bit_flag[pos] != 0;
+      const double v = ld_stream(C.val + pos) * ldx(C.x, ld_stream(C.col + pos));
+      if (f) {
+        if (seen == 0) head = sum;
+        else csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum);
+        ++seen;
+        sum = 0.0;
+      }
+      sum += v;
+    }
+  }
+  const bool F = seen > 0;
+  if (!F) head = sum;
+  // R_j = H_j + (F_j ? 0 : R_{j+1}): segmented suffix sum of heads.
+  double rv = head;
+  bool stop = F;
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, rv, d, W);
+    bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d, W) != 0;
+    if (!stop && j + d < W) {
+      rv += ov;
+      stop = ostop;
+    }
+  }
+  double right = __shfl_down_sync(0xffffffffu, rv, 1, W);
+  if (j == W - 1) right = 0.0;
+  if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
+}
+
+// Same algorithm with a compile-time sigma: each lane issues its S flag,
+// column and value loads back to back, then S independent x gathers, so a
+// warp keeps 32*S gathers in flight (random-column matrices are bound by the
+// L1TEX wavefront rate of these gathers, ~2 cycles per distinct line).
+template <int W, int S, bool PARTIAL>
+__global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane % W;
+  const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
+  const bool active = group < t_end;
+  const int64_t t = active ? group : t_begin;
+  const int64_t tile0 = t * static_cast<int64_t>(W) * S;
+  const double sc = load_scale(C.scale_p);
+  uint32_t fmask = 0;
+  int32_t cidx[S];
+  double v[S];
+  if (!PARTIAL) {
+    const int64_t base = tile0 + j;
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        fmask |= (C.bit_flag[base + i * W] ? 1u : 0u) << i;
+        cidx[i] = ld_stream(C.col + base + i * W);
+        v[i] = ld_stream(C.val + base + i * W);
+      }
+#pragma unroll
+      for (int i = 0; i < S; ++i) v[i] *= ldx(C.x, cidx[i]);
+    }
+  } else {
+    // trailing partial tile: row-major over occupied cells (formats.py:24-25)
+    const int64_t m = C.nnz - tile0;
+    const int q = static_cast<int>(m / S), rem = static_cast<int>(m % S);
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const bool ok = active && static_cast<int64_t>(j) * S + i < m;
+      const int64_t pos = tile0 + static_cast<int64_t>(i) * q + (i < rem ? i : rem) + j;
+      fmask |= (ok && C.bit_flag[pos] ? 1u : 0u) << i;
+      v[i] = ok ? C.val[pos] * ldx(C.x, C.col[pos]) : 0.0;
+    }
+  }
+  const uint32_t aux = active ? C.aux[t] : 0u;
+  const int nflags = __popc(fmask);
+  int incl = nflags;
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, d, W);
+    if (j >= d) incl += o;
+  }
+  const int seg_base = incl - nflags;
+  double head = 0.0, sum = 0.0;
+  int seen = 0;
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      if ((fmask >> i) & 1u) {
+        if (seen == 0) head = sum;
+        else csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum);
+        ++seen;
+        sum = 0.0;
+      }
+      sum += v[i];
+    }
+  }
+  const bool F = seen > 0;
+  if (!F) head = sum;
+  double rv = head;
+  bool stop = F;
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, rv, d, W);
+    bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d, W) != 0;
+    if (!stop && j + d < W) {
+      rv += ov;
+      stop = ostop;
+    }
+  }
+  double right = __shfl_down_sync(0xffffffffu, rv, 1, W);
+  if (j == W - 1) right = 0.0;
+  if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
+}
+
+// TMA-staged fast path for omega == 32, sigma <= 16: a CTA of 8 warps owns 8
+// consecutive full tiles, which are contiguous in stored order, so three bulk
+// copies (values, columns, flags; L2 evict_first) stage them; products are
+// formed CTA-wide with 16 independent x gathers per thread (L2 evict_last);
+// each warp then runs the column-segmented sum of one tile from shared memory.
+constexpr int C5_TPB = 8;
+constexpr int C5_MAX_ENTRIES = C5_TPB * 32 * 16;
+
+struct Csr5TmaSmem {
+  double vals[C5_MAX_ENTRIES];
+  int32_t cols[C5_MAX_ENTRIES];
+  uint8_t flags[C5_MAX_ENTRIES];
+  uint64_t bar;
+};
+
+__global__ void __launch_bounds__(256) k_csr5_tma(Csr5Ctx C, int64_t full_tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Csr5TmaSmem& sm = *reinterpret_cast<Csr5TmaSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sigma = C.sigma;
+  const int tile = 32 * sigma;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * C5_TPB;
+  const int ntile = full_tiles - t0 < C5_TPB ? static_cast<int>(full_tiles - t0) : C5_TPB;
+  const int cnt = ntile * tile;
+  const int64_t e0 = t0 * tile;
+  if (tid == 0) {
+    mbar_init(&sm.bar, 1);
+    const uint64_t pol = policy_evict_first();
+    mbar_arrive_expect_tx(&sm.bar, static_cast<uint32_t>(cnt) * 13u);
+    bulk_g2s(sm.vals, C.val + e0, cnt * 8u, &sm.bar, pol);
+    bulk_g2s(sm.cols, C.col + e0, cnt * 4u, &sm.bar, pol);
+    bulk_g2s(sm.flags, C.bit_flag + e0, static_cast<uint32_t>(cnt), &sm.bar, pol);
+  }
+  __syncthreads();
+  mbar_wait(&sm.bar, 0);
+  {
+    const uint64_t pol_x = policy_evict_last();
+    constexpr int PER = C5_MAX_ENTRIES / 256;
+    double p[PER];
+#pragma unroll
+    for (int it = 0; it < PER; ++it) {
+      const int e = tid + it * 256;
+      p[it] = e < cnt ? ld_hint(C.x + sm.cols[e], pol_x) : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < PER; ++it) {
+      const int e = tid + it * 256;
+      if (e < cnt) sm.vals[e] *= p[it];
+    }
+  }
+  __syncthreads();
+  if (warp >= ntile) return;  // whole warps only: shuffles below stay full-mask
+  const int64_t t = t0 + warp;
+  const uint32_t aux = C.aux[t];
+  const double sc = load_scale(C.scale_p);
+  const int base = warp * tile;
+  int nflags = 0;
+  for (int i = 0; i < sigma; ++i) nflags += sm.flags[base + i * 32 + lane] ? 1 : 0;
+  int incl = nflags;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  const int seg_base = incl - nflags;
+  double head = 0.0, sum = 0.0;
+  int seen = 0;
+  for (int i = 0; i < sigma; ++i) {
+    const int idx = base + i * 32 + lane;
+    if (sm.flags[idx]) {
+      if (seen == 0) head = sum;
+      else csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum);
+      ++seen;
+      sum = 0.0;
+    }
+    sum += sm.vals[idx];
+  }
+  const bool F = seen > 0;
+  if (!F) head = sum;
+  double rv = head;
+  bool stop = F;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, rv, d);
+    bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d) != 0;
+    if (!stop && lane + d < 32) {
+      rv += ov;
+      stop = ostop;
+    }
+  }
+  double right = __shfl_down_sync(0xffffffffu, rv, 1);
+  if (lane == 31) right = 0.0;
+  if (F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
+}
+
+__global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ aux,
+                             const double* __restrict__ carry, double* __restrict__ y) {
+  // chains of continuation tiles, folded warp-cooperatively as in k_merge_fixup
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w0 = warp_id * 32; w0 < num_tiles; w0 += nwarps * 32) {
+    const int64_t t = w0 + lane;
+    const bool cont = t < num_tiles && (aux[t] & 0x80000000u);
+    const int32_t r = cont ? tile_ptr[t] : -1;
+    const bool start = cont && !(t > 0 && (aux[t - 1] & 0x80000000u) && tile_ptr[t - 1] == r);
+    unsigned starts = __ballot_sync(0xffffffffu, start);
+    while (starts) {
+      const int l = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int32_t key = __shfl_sync(0xffffffffu, r, l);
+      double acc = 0.0;
+      for (int64_t b = w0 + l;; b += 32) {
+        const int64_t tt = b + lane;
+        const bool in = tt < num_tiles && (aux[tt] & 0x80000000u) && tile_ptr[tt] == key;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        const int len = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+        if (lane < len) acc += carry[tt];
+        if (len < 32) break;
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) y[key] = y[key] + acc;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma, const int32_t* tile_ptr,
+                               const uint8_t* bit_flag, const int32_t* col, const double* val, const uint32_t* tile_aux,
+                               const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x,
+                               double* y, const double* scale, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n_rows <= 0) return;
+    if (nnz == 0) {
+      SPMVB_CUDA(cudaMemsetAsync(y, 0, n_rows * sizeof(double), s));
+      return;
+    }
+    if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
+              nonempty_rows, carry, x, y, scale};
+    const int64_t tile = static_cast<int64_t>(omega) * sigma;
+    const int64_t num_tiles = (nnz + tile - 1) / tile;
+    const int64_t full = nnz / tile;
+    int64_t generic_begin = 0;
+    auto warp_launch = [&](auto kern, int W) {
+      int64_t threads = full * W;
+      kern<<<grid_for(threads, 256), 256, 0, s>>>(C, full);
+      SPMVB_LAUNCHED("k_csr5_warp");
+      generic_begin = full;
+    };
+    const bool tma_ok = omega == 32 && sigma <= 16 && aligned16(val) && aligned16(col) && aligned16(bit_flag);
+    // Kernel variant (experiments): SPMVB_CSR5_KERNEL=tma selects the
+    // TMA-staged kernel; the default is the register-unrolled warp kernel.
+    const char* variant = getenv("SPMVB_CSR5_KERNEL");
+    const bool want_tma = variant && variant[0] == 't';
+    auto warp_s_launch = [&](auto kern, auto kern_partial, int W) {  // full tiles, then the partial one
+      if (full > 0) {
+        kern<<<grid_for(full * W, 256), 256, 0, s>>>(C, 0, full);
+        SPMVB_LAUNCHED("k_csr5_warp_s");
+      }
+      if (num_tiles > full) {
+        kern_partial<<<1, 32, 0, s>>>(C, full, num_tiles);
+        SPMVB_LAUNCHED("k_csr5_warp_s_partial");
+      }
+      generic_begin = num_tiles;
+    };
+    if (!want_tma && (sigma == 16 || sigma == 8) &&
+        (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
+      if (sigma == 16) {
+        switch (omega) {
+          case 32: warp_s_launch(k_csr5_warp_s<32, 16, false>, k_csr5_warp_s<32, 16, true>, 32); break;
+          case 16: warp_s_launch(k_csr5_warp_s<16, 16, false>, k_csr5_warp_s<16, 16, true>, 16); break;
+          case 8: warp_s_launch(k_csr5_warp_s<8, 16, false>, k_csr5_warp_s<8, 16, true>, 8); break;
+          default: warp_s_launch(k_csr5_warp_s<4, 16, false>, k_csr5_warp_s<4, 16, true>, 4); break;
+        }
+      } else {
+        switch (omega) {
+          case 32: warp_s_launch(k_csr5_warp_s<32, 8, false>, k_csr5_warp_s<32, 8, true>, 32); break;
+          case 16: warp_s_launch(k_csr5_warp_s<16, 8, false>, k_csr5_warp_s<16, 8, true>, 16); break;
+          case 8: warp_s_launch(k_csr5_warp_s<8, 8, false>, k_csr5_warp_s<8, 8, true>, 8); break;
+          default: warp_s_launch(k_csr5_warp_s<4, 8, false>, k_csr5_warp_s<4, 8, true>, 4); break;
+        }
+      }
+    } else if (want_tma && tma_ok && full > 0) {
+      const size_t smem = sizeof(Csr5TmaSmem);
+      SPMVB_CUDA(cudaFuncSetAttribute(k_csr5_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_csr5_tma<<<static_cast<unsigned>((full + C5_TPB - 1) / C5_TPB), 256, smem, s>>>(C, full);
+      SPMVB_LAUNCHED("k_csr5_tma");
+      generic_begin = full;
+    } else if (sigma <= 1024 && full > 0) {
+      switch (omega) {
+        case 32: warp_launch(k_csr5_warp<32>, 32); break;
+        case 16: warp_launch(k_csr5_warp<16>, 16); break;
+        case 8: warp_launch(k_csr5_warp<8>, 8); break;
+        case 4: warp_launch(k_csr5_warp<4>, 4); break;
+        case 2: warp_launch(k_csr5_warp<2>, 2); break;
+        default: break;
+      }
+    }
+    if (generic_begin < num_tiles) {
+      k_csr5_generic<<<grid_for(num_tiles - generic_begin, 128, 148 * 64), 128, 0, s>>>(C, generic_begin, num_tiles);
+      SPMVB_LAUNCHED("k_csr5_generic");
+    }
+    if (num_tiles > 1) {
+      k_csr5_fixup<<<grid_for(num_tiles, 256, 148 * 8), 256, 0, s>>>(num_tiles, tile_ptr, tile_aux, carry, y);
+      SPMVB_LAUNCHED("k_csr5_fixup");
+    }
+  });
+}
+
