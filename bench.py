@@ -224,7 +224,7 @@ def run_ours(args):
             t0 = time.perf_counter()
             m = sp.convert(tag, shard, **kw)
             if tag in ("csr", "hyb"):
-                m.merge_plan()
+                m.chunk_plan()
             torch.cuda.synchronize()
             rec["convert_ms"] = (time.perf_counter() - t0) * 1e3
         except (sp.ConversionError, MemoryError, RuntimeError) as exc:

@@ -64,19 +64,20 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_sell_to_coo": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_hyb_plan": (c_int, [c_i64, vp, c_i64, c_i64, vp, P_i64, vp]),
     "spmvb_hyb_fill": (c_int, [c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "spmvb_csr_merge_tiles": (c_i64, [c_i64, c_i64]),
-    "spmvb_csr_merge_plan": (c_int, [c_i64, c_i64, vp, vp, vp, vp]),
-    "spmvb_spmv_csr": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvb_csr_chunk_size": (c_i64, []),
+    "spmvb_csr_chunks": (c_i64, [c_i64]),
+    "spmvb_csr_chunk_plan": (c_int, [c_i64, c_i64, vp, vp, vp]),
+    "spmvb_spmv_csr": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvb_spmv_hyb": (
+        c_int,
+        [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+    ),
     "spmvb_spmv_csr5": (
         c_int,
         [c_i64, c_i64, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
     ),
     "spmvb_spmv_ell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp]),
     "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "spmvb_spmv_hyb": (
-        c_int,
-        [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
-    ),
     "spmvb_sumsq": (c_int, [vp, c_i64, vp, vp]),
     "spmvb_inv_sqrt": (c_int, [vp, vp, vp]),
     "spmvb_csr_features": (c_int, [c_i64, c_i64, c_i64, vp, P_dbl, vp]),

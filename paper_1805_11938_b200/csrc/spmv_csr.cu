@@ -1,0 +1,290 @@
+// CSR SpMV by nnz chunks with on-the-fly segment flags (reference
+// kernels.py:76-95 spmv_csr), and the HYB kernel built on it
+// (kernels.py:177-199 spmv_hyb: ELL part + COO tail reduced through the
+// tail's row pointer).
+//
+// A warp owns a chunk of CH = 32*S consecutive nonzeros:
+//  1. coalesced (lane-striped) loads of S column/value pairs per lane, S
+//     independent x gathers in flight per lane, products into shared memory;
+//  2. the rows whose first entry lies in the chunk are scanned 32 at a time
+//     (chunk_row[] from the analysis step): a non-empty row marks its start
+//     position with its row id; an empty row is written (0, or its ELL part);
+//  3. each lane takes S consecutive products (a CSR5-like column of the
+//     chunk) and sums segments; a warp-shuffle suffix scan joins segments
+//     that cross lanes; segment sums are written to y.
+// Entries before the chunk's first row start continue a row owned by an
+// earlier chunk: their sum is the chunk's carry, folded by k_chunk_fixup in
+// ascending chunk order (deterministic, no floating-point atomics).
+#include "spmv_common.cuh"
+
+using namespace spmvb;
+
+namespace {
+
+constexpr int CK_WARPS = 8;
+
+// chunk_row[c] = first row r with ptr[r] >= c*CH (c < nchunks); chunk_row[nchunks] = n_rows.
+__global__ void k_chunk_plan(int64_t n_rows, int64_t nnz, int64_t ch, const int32_t* __restrict__ ptr,
+                             int64_t nchunks, int32_t* __restrict__ chunk_row) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c <= nchunks;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (c == nchunks) {
+      chunk_row[c] = static_cast<int32_t>(n_rows);
+      continue;
+    }
+    const int64_t v = c * ch;
+    int64_t lo = 0, hi = n_rows;  // lower_bound over ptr[0..n_rows)
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (ptr[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    chunk_row[c] = static_cast<int32_t>(lo);
+  }
+}
+
+template <int S>
+struct ChunkSmem {
+  static constexpr int CH = 32 * S;
+  double prod[CK_WARPS][CH + CH / S];  // skewed: entry e at e + e / S (conflict-free both ways)
+  int32_t seg[CK_WARPS][CH];           // row id of a row starting at position e, else -1
+};
+
+template <bool HAS_ELL>
+__device__ __forceinline__ double ell_row(int64_t n_rows, int64_t r, int64_t ell_k, const int32_t* __restrict__ ell_idx,
+                                          const double* __restrict__ ell_val, const double* __restrict__ x) {
+  double e = 0.0;
+  if (HAS_ELL)
+    for (int64_t j = 0; j < ell_k; ++j) {
+      const int64_t o = j * n_rows + r;
+      e = __dadd_rn(e, __dmul_rn(ld_stream(ell_val + o), ldx(x, ld_stream(ell_idx + o))));
+    }
+  return e;
+}
+
+template <int S, bool HAS_ELL>
+__global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
+    int64_t n_rows, int64_t nnz, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+    const double* __restrict__ val, const int32_t* __restrict__ chunk_row, int64_t nchunks,
+    int32_t* __restrict__ carry_row, double* __restrict__ carry_val, const double* __restrict__ x,
+    double* __restrict__ y, const double* __restrict__ scale_p, int64_t ell_k, const int32_t* __restrict__ ell_idx,
+    const double* __restrict__ ell_val) {
+  constexpr int CH = 32 * S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ChunkSmem<S>& sm = *reinterpret_cast<ChunkSmem<S>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * CK_WARPS + w;
+  if (c >= nchunks) return;  // whole warps only
+  const int64_t k0 = c * CH;
+  const int cnt = static_cast<int>(nnz - k0 < CH ? nnz - k0 : CH);
+  double* prod = sm.prod[w];
+  int32_t* seg = sm.seg[w];
+
+  // 1. products, lane-striped (coalesced) with S gathers in flight per lane
+  {
+    int32_t ci[S];
+    double vi[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const int e = i * 32 + lane;
+      ci[i] = e < cnt ? ld_stream(col + k0 + e) : 0;
+      vi[i] = e < cnt ? ld_stream(val + k0 + e) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const int e = i * 32 + lane;
+      prod[e + e / S] = e < cnt ? vi[i] * ldx(x, ci[i]) : 0.0;
+      seg[e] = -1;
+    }
+  }
+  __syncwarp();
+  // 2. rows starting in this chunk
+  const double sc = load_scale(scale_p);
+  const int32_t ra = chunk_row[c], rb = chunk_row[c + 1];
+  for (int64_t r = ra + lane; r < rb; r += 32) {
+    const int32_t s0 = ptr[r], s1 = ptr[r + 1];
+    // HYB: every owned row's ELL part is formed here (lanes on consecutive
+    // rows: coalesced column-major ELL loads); a row with tail entries parks
+    // it unscaled in y[r] for the lane that closes the row's segment.
+    const double e = HAS_ELL ? ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0;
+    if (s1 > s0) {
+      seg[s0 - k0] = static_cast<int32_t>(r);
+      if (HAS_ELL) y[r] = e;
+    } else {
+      y[r] = sc * e;
+    }
+  }
+  __syncwarp();  // also orders the parked y[r] stores before the reads below
+  // 3. lane-contiguous segments
+  uint32_t fmask = 0;
+  double v[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    const int e = lane * S + i;
+    v[i] = prod[e + e / S];
+    fmask |= (seg[e] >= 0 ? 1u : 0u) << i;
+  }
+  double head = 0.0, sum = 0.0;
+  int open_row = -1;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    if ((fmask >> i) & 1u) {
+      if (open_row < 0) head = sum;
+      else y[open_row] = sc * (HAS_ELL ? y[open_row] + sum : sum);
+      open_row = seg[lane * S + i];
+      sum = 0.0;
+    }
+    sum += v[i];
+  }
+  const bool F = open_row >= 0;
+  if (!F) head = sum;
+  // R_l = H_l + (F_l ? 0 : R_{l+1}): segmented suffix sum of lane heads
+  double rv = head;
+  bool stop = F;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, rv, d);
+    const bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d) != 0;
+    if (!stop && lane + d < 32) {
+      rv += ov;
+      stop = ostop;
+    }
+  }
+  double right = __shfl_down_sync(0xffffffffu, rv, 1);
+  if (lane == 31) right = 0.0;
+  if (F) y[open_row] = sc * (HAS_ELL ? y[open_row] + (sum + right) : sum + right);
+  if (lane == 0) {
+    // leading entries continue row ra - 1 unless a row starts at position 0
+    const bool cont = !(fmask & 1u);
+    carry_row[c] = cont ? ra - 1 : -1;
+    carry_val[c] = cont ? rv : 0.0;
+  }
+}
+
+// Folds every chain of chunk carry-outs (consecutive chunks whose carry row is
+// the same) into its row: one warp per 32 chunks finds the chain starts, each
+// chain is summed by the whole warp 32 chunks per step with a fixed tree.
+__global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row, const double* __restrict__ carry_val,
+                              double* __restrict__ y, const double* __restrict__ scale_p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t w0 = warp_id * 32; w0 < num; w0 += nwarps * 32) {
+    const int64_t cc = w0 + lane;
+    const int32_t r = cc < num ? carry_row[cc] : -1;
+    const bool start = r >= 0 && !(cc > 0 && carry_row[cc - 1] == r);
+    unsigned starts = __ballot_sync(0xffffffffu, start);
+    while (starts) {
+      const int l = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int32_t key = __shfl_sync(0xffffffffu, r, l);
+      double acc = 0.0;
+      for (int64_t b = w0 + l;; b += 32) {
+        const int64_t t = b + lane;
+        const bool in = t < num && carry_row[t] == key;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        const int len = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+        if (lane < len) acc += carry_val[t];
+        if (len < 32) break;
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) y[key] += load_scale(scale_p) * acc;
+    }
+  }
+}
+
+// y = ELL part only (HYB whose tail is empty)
+__global__ void k_ell_only(int64_t n_rows, int64_t ell_k, const int32_t* __restrict__ ell_idx,
+                           const double* __restrict__ ell_val, const double* __restrict__ x, double* __restrict__ y,
+                           const double* __restrict__ scale_p) {
+  const double sc = load_scale(scale_p);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[r] = sc * ell_row<true>(n_rows, r, ell_k, ell_idx, ell_val, x);
+}
+
+template <int S, bool HAS_ELL>
+void launch_chunk_t(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
+                    const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x, double* y,
+                    const double* scale, int64_t ell_k, const int32_t* ell_idx, const double* ell_val,
+                    cudaStream_t s) {
+  constexpr int CH = 32 * S;
+  const int64_t nchunks = (nnz + CH - 1) / CH;
+  const size_t smem = sizeof(ChunkSmem<S>);
+  SPMVB_CUDA(cudaFuncSetAttribute(k_spmv_chunk<S, HAS_ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_spmv_chunk<S, HAS_ELL><<<static_cast<unsigned>((nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem, s>>>(
+      n_rows, nnz, ptr, col, val, chunk_row, nchunks, carry_row, carry_val, x, y, scale, ell_k, ell_idx, ell_val);
+  SPMVB_LAUNCHED("k_spmv_chunk");
+  if (nchunks > 1) {
+    k_chunk_fixup<<<grid_for(nchunks, 256, 148 * 8), 256, 0, s>>>(nchunks, carry_row, carry_val, y, scale);
+    SPMVB_LAUNCHED("k_chunk_fixup");
+  }
+}
+
+int chunk_s() {
+  const char* e = getenv("SPMVB_CSR_CHUNK_S");
+  return (e && e[0] == '1') ? 16 : 8;  // S = 8 measured faster on C1-C5 (occupancy)
+}
+
+void launch_chunk(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
+                  const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x, double* y,
+                  const double* scale, int64_t ell_k, const int32_t* ell_idx, const double* ell_val, cudaStream_t s) {
+  if (n_rows <= 0) return;
+  if (nnz == 0) {
+    if (ell_k > 0) {
+      k_ell_only<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, ell_k, ell_idx, ell_val, x, y, scale);
+      SPMVB_LAUNCHED("k_ell_only");
+    } else {
+      SPMVB_CUDA(cudaMemsetAsync(y, 0, n_rows * sizeof(double), s));
+    }
+    return;
+  }
+  const int S = chunk_s();
+  if (ell_k > 0) {
+    if (S == 8) launch_chunk_t<8, true>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, ell_k, ell_idx, ell_val, s);
+    else launch_chunk_t<16, true>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, ell_k, ell_idx, ell_val, s);
+  } else {
+    if (S == 8) launch_chunk_t<8, false>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, 0, nullptr, nullptr, s);
+    else launch_chunk_t<16, false>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, 0, nullptr, nullptr, s);
+  }
+}
+
+}  // namespace
+
+extern "C" int64_t spmvb_csr_chunk_size(void) { return 32 * chunk_s(); }
+
+extern "C" int64_t spmvb_csr_chunks(int64_t nnz) {
+  const int64_t ch = 32 * chunk_s();
+  return nnz > 0 ? (nnz + ch - 1) / ch : 0;
+}
+
+extern "C" int spmvb_csr_chunk_plan(int64_t n_rows, int64_t nnz, const int32_t* ptr, int32_t* chunk_row,
+                                    void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    const int64_t ch = 32 * chunk_s();
+    const int64_t nchunks = nnz > 0 ? (nnz + ch - 1) / ch : 0;
+    k_chunk_plan<<<grid_for(nchunks + 1, 256, 148 * 16), 256, 0, s>>>(n_rows, nnz, ch, ptr, nchunks, chunk_row);
+    SPMVB_LAUNCHED("k_chunk_plan");
+  });
+}
+
+extern "C" int spmvb_spmv_csr(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                                      const double* val, const int32_t* chunk_row, int32_t* carry_row,
+                                      double* carry_val, const double* x, double* y, const double* scale,
+                                      void* stream) {
+  return guard([&] {
+    launch_chunk(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, 0, nullptr, nullptr,
+                 as_stream(stream));
+  });
+}
+
+extern "C" int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const double* ell_val,
+                                      int64_t tail_nnz, const int32_t* tail_ptr, const int32_t* tail_col,
+                                      const double* tail_val, const int32_t* chunk_row, int32_t* carry_row,
+                                      double* carry_val, const double* x, double* y, const double* scale,
+                                      void* stream) {
+  return guard([&] {
+    launch_chunk(n_rows, tail_nnz, tail_ptr, tail_col, tail_val, chunk_row, carry_row, carry_val, x, y, scale, k,
+                 ell_idx, ell_val, as_stream(stream));
+  });
+}

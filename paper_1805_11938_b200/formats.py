@@ -14,7 +14,7 @@ coalesced and the attribute returns the reference's *logical* view:
   ``bit_flag`` is a bool tensor in stored order.
 
 Every conversion runs on the device (csrc/formats.cu, csrc/coo.cu).
-Kernel-side auxiliary data (merge-path tile coordinates, CSR5 tile words,
+Kernel-side auxiliary data (CSR chunk first-row tables, CSR5 tile words,
 the non-empty row list) is derived at conversion time or lazily on first
 use, like a cuSPARSE analysis buffer; it is not part of the reference
 arrays and does not change them.
@@ -84,28 +84,24 @@ def _row_stats(ptr_t: torch.Tensor, n_rows: int) -> tuple[int, int, int]:
     return int(out[0]), int(out[1]), int(out[2])
 
 
-class _MergePlan:
-    """Merge-path tile coordinates for a (ptr, nnz) pair, built once."""
+class _ChunkPlan:
+    """Per-chunk first-row table for the chunked CSR kernel, built once."""
 
     def __init__(self, ptr_t: torch.Tensor, n_rows: int, nnz: int):
         dev = ptr_t.device
-        self.tiles = int(LIB.spmvb_csr_merge_tiles(n_rows, nnz))
-        self.tile_row = _i32(self.tiles + 1, dev)
-        self.tile_nz = _i32(self.tiles + 1, dev)
-        if self.tiles:
+        self.chunk = int(LIB.spmvb_csr_chunk_size())
+        self.chunks = int(LIB.spmvb_csr_chunks(nnz))
+        self.chunk_row = _i32(self.chunks + 1, dev)
+        if n_rows:
             with torch.cuda.device(dev):
-                check(
-                    LIB.spmvb_csr_merge_plan(
-                        n_rows, nnz, ptr(ptr_t), ptr(self.tile_row), ptr(self.tile_nz), _lib.stream(dev)
-                    )
-                )
+                check(LIB.spmvb_csr_chunk_plan(n_rows, nnz, ptr(ptr_t), ptr(self.chunk_row), _lib.stream(dev)))
 
     def scratch(self, dev):
-        return _i32(max(self.tiles, 1), dev), _f64(max(self.tiles, 1), dev)
+        return _i32(max(self.chunks, 1), dev), _f64(max(self.chunks, 1), dev)
 
     @property
     def nbytes(self) -> int:
-        return 8 * (self.tiles + 1)
+        return 4 * (self.chunks + 1)
 
 
 class CsrMatrix:
@@ -117,7 +113,12 @@ class CsrMatrix:
         self.ptr = ptr
         self.indices = indices
         self.data = data
-        self._merge: _MergePlan | None = None
+        self._chunks: _ChunkPlan | None = None
+
+    def chunk_plan(self) -> _ChunkPlan:
+        if self._chunks is None:
+            self._chunks = _ChunkPlan(self.ptr, self.n_rows, self.nnz)
+        return self._chunks
 
     @property
     def nnz(self) -> int:
@@ -126,11 +127,6 @@ class CsrMatrix:
     @property
     def device(self) -> torch.device:
         return self.ptr.device
-
-    def merge_plan(self) -> _MergePlan:
-        if self._merge is None:
-            self._merge = _MergePlan(self.ptr, self.n_rows, self.nnz)
-        return self._merge
 
     def __repr__(self) -> str:
         return f"CsrMatrix({self.n_rows}x{self.n_cols}, nnz={self.nnz})"
@@ -288,14 +284,19 @@ class HybMatrix:
     """ELL part of width K plus a canonical COO tail (formats.py:156-177).
 
     ``tail_ptr`` (kernel-side) is the tail's per-row offset array, so the
-    tail is reduced by the merge-path kernel without atomics.
+    tail is reduced by the chunked CSR kernel without atomics.
     """
 
     def __init__(self, ell: EllMatrix, coo_tail: CooMatrix, tail_ptr: torch.Tensor):
         self.ell = ell
         self.coo_tail = coo_tail
         self.tail_ptr = tail_ptr
-        self._merge: _MergePlan | None = None
+        self._chunks: _ChunkPlan | None = None
+
+    def chunk_plan(self) -> _ChunkPlan:
+        if self._chunks is None:
+            self._chunks = _ChunkPlan(self.tail_ptr, self.n_rows, self.coo_tail.nnz)
+        return self._chunks
 
     n_rows = property(lambda self: self.ell.n_rows)
     n_cols = property(lambda self: self.ell.n_cols)
@@ -308,11 +309,6 @@ class HybMatrix:
     @property
     def device(self) -> torch.device:
         return self.tail_ptr.device
-
-    def merge_plan(self) -> _MergePlan:
-        if self._merge is None:
-            self._merge = _MergePlan(self.tail_ptr, self.n_rows, self.coo_tail.nnz)
-        return self._merge
 
     def __repr__(self) -> str:
         return f"HybMatrix({self.n_rows}x{self.n_cols}, K={self.k}, tail={self.coo_tail.nnz})"

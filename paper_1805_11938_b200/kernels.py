@@ -30,8 +30,8 @@ __all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_ell", "spmv
 
 def plan_row_blocks(n_rows: int, workers: int) -> list[tuple[int, int]]:
     """Host task plan of the reference CPU path (kernels.py:61-66); kept for
-    API compatibility.  The GPU kernels decompose by merge-path tiles,
-    CSR5 tiles or rows instead."""
+    API compatibility.  The GPU kernels decompose by nonzero chunks, CSR5
+    tiles or rows instead."""
     if n_rows == 0:
         return []
     block = max(1, n_rows // (4 * max(workers, 1)))
@@ -89,15 +89,15 @@ def _run(m, x, out, scale, launch):
 
 
 def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = A x for CSR via the merge-path kernel (kernels.py:76-95)."""
-    plan = m.merge_plan()
+    """y = A x for CSR via the chunked kernel (kernels.py:76-95)."""
+    plan = m.chunk_plan()
 
     def launch(xd, y, sp, s):
         cr, cv = plan.scratch(m.device)
         check(
             LIB.spmvb_spmv_csr(
-                m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.tile_row), ptr(plan.tile_nz),
-                ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
+                m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.chunk_row), ptr(cr), ptr(cv),
+                ptr(xd), ptr(y), sp, s,
             )
         )
 
@@ -145,15 +145,15 @@ def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
 
 def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None):
     """y = ELL part + COO tail (kernels.py:177-199), one fused kernel."""
-    plan = m.merge_plan()
+    t = m.coo_tail
+    plan = m.chunk_plan()
 
     def launch(xd, y, sp, s):
         cr, cv = plan.scratch(m.device)
-        t = m.coo_tail
         check(
             LIB.spmvb_spmv_hyb(
                 m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), t.nnz, ptr(m.tail_ptr), ptr(t.col),
-                ptr(t.data), ptr(plan.tile_row), ptr(plan.tile_nz), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
+                ptr(t.data), ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
             )
         )
 
