@@ -202,10 +202,17 @@ int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma, const int
 int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const double* x, double* y,
                    const double* scale, void* stream);
 
-/* spmv_sell (kernels.py:119-136); perm may be NULL for sigma == 0. */
+/* spmv_sell (kernels.py:119-136); perm may be NULL for sigma == 0.  Slices
+ * up to SPMVB_SELL_WIDE_COLS wide (or taller than 128 rows) are summed one
+ * thread per row, sequentially and without FMA: bit-identical to the
+ * reference.  Wider slices (power-law rows) are listed by
+ * spmvb_sell_wide_plan and summed by a CTA each (within tolerance). */
+#define SPMVB_SELL_WIDE_COLS 256
+int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out, int64_t* n_wide,
+                         void* stream);
 int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
-                    const int32_t* perm, const int32_t* idx, const double* val, const double* x, double* y,
-                    const double* scale, void* stream);
+                    const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
+                    const double* x, double* y, const double* scale, void* stream);
 
 /* ||y||^2 over n entries into *out (device), deterministic two-level sum.
  * Used by power iteration. */

@@ -45,6 +45,7 @@ __global__ void k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict
     const int64_t sl = p / c, local = p - sl * c;
     const int64_t rows_s = (sl + 1) * c <= n_rows ? c : n_rows - sl * c;
     const int64_t w = widths[sl];
+    if (w > SPMVB_SELL_WIDE_COLS && rows_s <= 128) continue;  // k_spmv_sell_wide's slice
     const int64_t o0 = slice_off[sl] + local;
     double acc = 0.0;
     int64_t j = 0;
@@ -68,7 +69,90 @@ __global__ void k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict
   }
 }
 
+// Wide slices (width > SPMVB_SELL_WIDE_COLS, power-law rows): one CTA per
+// slice, 256/rows threads per row each summing every (256/rows)-th column
+// (coalesced: consecutive threads read consecutive column-major cells), then
+// a fixed-order per-row sum of the thread partials (deterministic; not the
+// reference's sequential order, so within tolerance rather than bit-exact).
+__global__ void __launch_bounds__(256) k_spmv_sell_wide(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide,
+                                                        const int64_t* __restrict__ widths,
+                                                        const int64_t* __restrict__ slice_off,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                        const double* __restrict__ x, double* __restrict__ y,
+                                                        const double* __restrict__ scale_p) {
+  __shared__ double red[256];
+  const int t = threadIdx.x;
+  const int64_t sl = wide[blockIdx.x];
+  const int rows_s = static_cast<int>((sl + 1) * c <= n_rows ? c : n_rows - sl * c);
+  const int nsub = 256 / rows_s;
+  const int sub = t / rows_s, l = t - sub * rows_s;
+  const int64_t w = widths[sl];
+  const int64_t base = slice_off[sl];
+  double acc = 0.0;
+  if (sub < nsub) {
+    int64_t j = sub;
+    for (; j + 3 * nsub < w; j += 4 * nsub) {
+      const int64_t o = base + j * rows_s + l, st = static_cast<int64_t>(nsub) * rows_s;
+      const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + st);
+      const double v2 = ld_stream(val + o + 2 * st), v3 = ld_stream(val + o + 3 * st);
+      const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + st);
+      const int32_t c2 = ld_stream(idx + o + 2 * st), c3 = ld_stream(idx + o + 3 * st);
+      acc += v0 * ldx(x, c0);
+      acc += v1 * ldx(x, c1);
+      acc += v2 * ldx(x, c2);
+      acc += v3 * ldx(x, c3);
+    }
+    for (; j < w; j += nsub) {
+      const int64_t o = base + j * rows_s + l;
+      acc += ld_stream(val + o) * ldx(x, ld_stream(idx + o));
+    }
+  }
+  red[t] = acc;
+  __syncthreads();
+  if (t < rows_s) {
+    double s = 0.0;
+    for (int k = 0; k < nsub; ++k) s += red[t + k * rows_s];
+    const int64_t p = sl * c + t;
+    const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
+    y[r] = scale_p ? load_scale(scale_p) * s : s;
+  }
+}
+
+__global__ void k_sell_mark_wide(const int64_t* __restrict__ widths, int64_t n_rows, int64_t c, int64_t n_slices,
+                                 uint8_t* __restrict__ flag) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n_slices;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t rows_s = (s + 1) * c <= n_rows ? c : n_rows - s * c;
+    flag[s] = (widths[s] > SPMVB_SELL_WIDE_COLS && rows_s <= 128) ? 1 : 0;
+  }
+}
+
 }  // namespace
+
+extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out,
+                                    int64_t* n_wide, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    *n_wide = 0;
+    if (n_rows <= 0 || c < 1) return;
+    const int64_t n_slices = (n_rows + c - 1) / c;
+    DevBuf<uint8_t> flag(n_slices, s);
+    k_sell_mark_wide<<<grid_for(n_slices, 256, 148 * 16), 256, 0, s>>>(widths, n_rows, c, n_slices, flag.get());
+    SPMVB_LAUNCHED("k_sell_mark_wide");
+    const uint8_t* f = flag.get();
+    DevBuf<int32_t> total(1, s);
+    exclusive_scan<int32_t>(
+        n_slices, [=] __device__(int64_t i) { return static_cast<int32_t>(f[i]); },
+        [=] __device__(int64_t i, int32_t v) {
+          if (f[i]) wide_out[v] = static_cast<int32_t>(i);
+        },
+        OpSum{}, 0, total.get(), s);
+    int32_t h = 0;
+    copy_to_host(&h, total.get(), 1, s);
+    *n_wide = h;
+  });
+}
 
 extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const double* x,
                               double* y, const double* scale, void* stream) {
@@ -81,13 +165,18 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
 }
 
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
-                               const int32_t* perm, const int32_t* idx, const double* val, const double* x, double* y,
-                               const double* scale, void* stream) {
+                               const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
+                               int64_t n_wide, const double* x, double* y, const double* scale, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
     k_spmv_sell<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_sell");
+    if (n_wide > 0) {
+      k_spmv_sell_wide<<<static_cast<unsigned>(n_wide), 256, 0, s>>>(n_rows, c, wide, widths, slice_off, perm, idx,
+                                                                     val, x, y, scale);
+      SPMVB_LAUNCHED("k_spmv_sell_wide");
+    }
   });
 }
 

@@ -246,6 +246,19 @@ class SellMatrix:
         self.flat_data = flat_data
         self.row_nnz_perm = row_nnz_perm
         self._host = None
+        self._wide = None
+
+    def wide_plan(self):
+        """Slices wider than SPMVB_SELL_WIDE_COLS (kernel-side, built once)."""
+        if self._wide is None:
+            n_slices = self.n_slices
+            lst = _i32(max(n_slices, 1), self.device)
+            cnt = ctypes.c_int64()
+            with torch.cuda.device(self.device):
+                check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), ptr(lst), ctypes.byref(cnt),
+                                               _lib.stream(self.device)))
+            self._wide = (lst, int(cnt.value))
+        return self._wide
 
     def _host_layout(self):
         if self._host is None:

@@ -78,6 +78,15 @@ def select_format(
     return tag, convert(tag, a, omega=omega, sigma=sigma, sell_c=sell_c, sell_sigma=sell_sigma)
 
 
+def _float(tok: str) -> float:
+    # The reference writer formats scale extremes with repr(); under numpy 2
+    # that yields "np.float64(25.0)" (model.py:338-339), which the reference
+    # reader cannot parse back.  Accept both spellings.
+    if tok.startswith("np.float64(") and tok.endswith(")"):
+        tok = tok[len("np.float64("):-1]
+    return float(tok)
+
+
 def _parse_line(toks: list[str], nodes: dict, mins: np.ndarray, maxs: np.ndarray) -> None:
     kind = toks[0]
     if kind == "node" and len(toks) == 7 and toks[2] == "split":
@@ -89,8 +98,8 @@ def _parse_line(toks: list[str], nodes: dict, mins: np.ndarray, maxs: np.ndarray
         f = int(toks[1])
         if not 0 <= f < N_FEATURES:
             raise ValueError(f"feature index {f}")
-        mins[f] = float(toks[2])
-        maxs[f] = float(toks[3])
+        mins[f] = _float(toks[2])
+        maxs[f] = _float(toks[3])
     else:
         raise ValueError("unrecognized line")
 

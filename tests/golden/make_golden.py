@@ -145,6 +145,29 @@ def main() -> None:
             sk.bandwidth_estimate("sell", sk.to_sell(a, 4, 0), 1.0),
             sk.bandwidth_estimate("hyb", mh, 1.0),
         ])
+    # A format-selection model trained by the reference itself (train_tree on
+    # its helpers' synthetic cost-model corpus), saved in its text format,
+    # plus the tag its predict() assigns to every case above.
+    import io
+
+    sys.path.insert(0, str(REF.parent / "tests"))
+    import helpers  # reference test helpers (cost-model corpus)
+
+    corpus = helpers.make_cost_corpus(7, 60)
+    samples = []
+    for mid, a in corpus:
+        f = sk.extract_features(a)
+        best = min(sk.FormatTag, key=lambda t: (helpers.cost_model(f, t), list(sk.FormatTag).index(t)))
+        samples.append(sk.LabeledSample(mid, f, best))
+    model = sk.train_tree(samples, max_depth=6, min_samples_leaf=2)
+    buf = io.StringIO()
+    sk.save_model(model, buf)
+    out["__model__"] = np.array(buf.getvalue())
+    for name in names:
+        nr, nc = (int(t) for t in out[name + "/shape"])
+        if nr and nc:
+            a = sk.canonicalize(out[name + "/row"], out[name + "/col"], out[name + "/data"], nr, nc)
+            out[name + "/predicted"] = np.array(sk.predict(model, sk.extract_features(a)).value)
     out["__names__"] = np.array(names)
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(names)} cases)")

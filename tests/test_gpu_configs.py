@@ -114,7 +114,11 @@ def test_config_parity(sp, name):
         assert np.array_equal(h(ms.perm), so.perm) and np.array_equal(h(ms.widths), so.widths)
         flat = np.concatenate([d.ravel(order="F") for d in so.data])
         assert h(ms.flat_data).tobytes() == flat.tobytes()
-        assert h(sp.spmv("sell", ms, xd)).tobytes() == port.spmv_sell(so, n, x).tobytes()
+        ys = sp.spmv("sell", ms, xd)
+        if int(so.widths.max()) <= 256:  # every slice summed sequentially: bit-identical
+            assert h(ys).tobytes() == port.spmv_sell(so, n, x).tobytes()
+        else:  # wide power-law slices are split across a CTA (SPMVB_SELL_WIDE_COLS)
+            check_within(ys, ref, bound)
 
     K, hi, hd, hn, tail = port.to_hyb(row, col, val, n)
     mh = sp.to_hyb(m)

@@ -213,3 +213,26 @@ def test_matrix_market_round_trip(sp, rng):
     buf = io.StringIO()
     sp.write_matrix_market(b, buf)
     assert sp.coo_equal(sp.read_matrix_market(buf.getvalue().encode()), b)
+
+
+def test_select_format_matches_reference(sp, golden):
+    """select_format (model.py:305-319): GPU features -> host tree descent ->
+    GPU convert, with a model trained and saved by the reference."""
+    model = sp.load_model(io.StringIO(str(golden.d["__model__"])))
+    for name in golden.names:
+        g = golden.case(name)
+        if "predicted" not in g:
+            continue
+        nr, nc = (int(t) for t in g["shape"])
+        a = sp.canonicalize(g["row"], g["col"], g["data"], nr, nc)
+        tag, m = sp.select_format(a, model)
+        assert tag.value == str(g["predicted"]), name
+        assert sp.coo_equal(sp.to_coo(m), a), name
+
+
+def test_extra_features_against_oracle(sp, rng):
+    for _ in range(10):
+        rr, cc, vv, nr, nc = random_triplets(rng, max_dim=200)
+        a = sp.canonicalize(rr, cc, vv, nr, nc)
+        r, c, v = port.canonicalize(rr, cc, vv, nr, nc)
+        assert sp.extract_extra_features(a) == port.extra_features(r, c, nr, nc)

@@ -167,3 +167,26 @@ def test_synth_ref_rmat_is_deterministic_and_deduplicated():
     assert (v > 0).all() and (v <= 1).all()
     # the quadrant skew (a=0.57) makes low row ids denser
     assert (r < 128).mean() > 0.6
+
+
+def test_model_loading_and_prediction_match_reference(golden):
+    """model.load_model parses the reference's model file; model.predict (host
+    tree descent, model.py:216-223) reproduces the reference's predictions on
+    the reference's own feature vectors."""
+    import io
+
+    from paper_1805_11938_b200.features import FeatureVector
+    from paper_1805_11938_b200.model import load_model, predict
+
+    model = load_model(io.StringIO(str(golden.d["__model__"])))
+    checked = 0
+    for name in golden.names:
+        g = golden.case(name)
+        if "predicted" not in g:
+            continue
+        f = g["features"]
+        fv = FeatureVector(int(f[0]), int(f[1]), float(f[2]), int(f[3]), int(f[4]), float(f[5]), float(f[6]),
+                           float(f[7]))
+        assert predict(model, fv).value == str(g["predicted"]), name
+        checked += 1
+    assert checked >= 20
