@@ -170,24 +170,27 @@ int spmvb_sell_to_coo(int64_t n_rows, int64_t c, const int32_t* perm, const int6
 /* ======================================================================== */
 
 /* CSR and HYB kernels work on chunks of spmvb_csr_chunk_size() consecutive
- * nonzeros (one warp each).  Analysis step (like a cuSPARSE buffer):
- * chunk_row[c] = first row whose first entry is at or after chunk c
- * (spmvb_csr_chunks(nnz) + 1 entries, the last = n_rows).
+ * nonzeros (one warp each).  Analysis step (like a cuSPARSE buffer): the
+ * ascending list of non-empty rows nz_rows[n_nz] (spmvb_csr_nonempty_rows;
+ * pass NULL and n_nz = n_rows when every row is non-empty) and
+ * chunk_row[c] = first index into that list whose row starts at or after
+ * chunk c (spmvb_csr_chunks(nnz) + 1 entries, the last = n_nz).
  * carry_row/carry_val: spmvb_csr_chunks(nnz) scratch entries. */
 int64_t spmvb_csr_chunk_size(void);
 int64_t spmvb_csr_chunks(int64_t nnz);
-int spmvb_csr_chunk_plan(int64_t n_rows, int64_t nnz, const int32_t* ptr, int32_t* chunk_row, void* stream);
+int spmvb_csr_chunk_plan(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* nz_rows, int64_t n_nz,
+                         int32_t* chunk_row, void* stream);
 /* spmv_csr (kernels.py:76-95). */
 int spmvb_spmv_csr(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
-                   const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x, double* y,
-                   const double* scale, void* stream);
+                   const int32_t* nz_rows, int64_t n_nz, const int32_t* chunk_row, int32_t* carry_row,
+                   double* carry_val, const double* x, double* y, const double* scale, void* stream);
 /* spmv_hyb (kernels.py:177-199): ELL part plus the COO tail, the tail reduced
- * through its row pointer (tail_ptr from spmvb_hyb_plan; chunk_row from
- * spmvb_csr_chunk_plan over (tail_ptr, tail_nnz)). */
+ * through its row pointer (tail_ptr from spmvb_hyb_plan; nz_rows/chunk_row
+ * from the analysis above over (tail_ptr, tail_nnz)). */
 int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const double* ell_val, int64_t tail_nnz,
-                   const int32_t* tail_ptr, const int32_t* tail_col, const double* tail_val, const int32_t* chunk_row,
-                   int32_t* carry_row, double* carry_val, const double* x, double* y, const double* scale,
-                   void* stream);
+                   const int32_t* tail_ptr, const int32_t* tail_col, const double* tail_val, const int32_t* nz_rows,
+                   int64_t n_nz, const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x,
+                   double* y, const double* scale, void* stream);
 
 /* spmv_csr5 (kernels.py:139-174). nonempty_rows may be NULL when every row is
  * non-empty. carry: num_tiles scratch doubles. */

@@ -66,11 +66,11 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_hyb_fill": (c_int, [c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_csr_chunk_size": (c_i64, []),
     "spmvb_csr_chunks": (c_i64, [c_i64]),
-    "spmvb_csr_chunk_plan": (c_int, [c_i64, c_i64, vp, vp, vp]),
-    "spmvb_spmv_csr": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvb_csr_chunk_plan": (c_int, [c_i64, c_i64, vp, vp, c_i64, vp, vp]),
+    "spmvb_spmv_csr": (c_int, [c_i64, c_i64, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_spmv_hyb": (
         c_int,
-        [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+        [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp],
     ),
     "spmvb_spmv_csr5": (
         c_int,

@@ -6,15 +6,17 @@
 // A warp owns a chunk of CH = 32*S consecutive nonzeros:
 //  1. coalesced (lane-striped) loads of S column/value pairs per lane, S
 //     independent x gathers in flight per lane, products into shared memory;
-//  2. the rows whose first entry lies in the chunk are scanned 32 at a time
-//     (chunk_row[] from the analysis step): a non-empty row marks its start
-//     position with its row id; an empty row is written (0, or its ELL part);
+//  2. the non-empty rows whose first entry lies in the chunk (a contiguous
+//     range of the non-empty row list, from the analysis step) mark their
+//     start positions with their row id;
 //  3. each lane takes S consecutive products (a CSR5-like column of the
 //     chunk) and sums segments; a warp-shuffle suffix scan joins segments
 //     that cross lanes; segment sums are written to y.
-// Entries before the chunk's first row start continue a row owned by an
-// earlier chunk: their sum is the chunk's carry, folded by k_chunk_fixup in
-// ascending chunk order (deterministic, no floating-point atomics).
+// Entries before the chunk's first row start continue the previous
+// non-empty row: their sum is the chunk's carry, folded by k_chunk_fixup in
+// ascending chunk order (deterministic, no floating-point atomics).  Empty
+// rows are written by one coalesced grid-stride pass (0, or for HYB the
+// row's ELL part), so a long run of empty rows never serialises one warp.
 #include "spmv_common.cuh"
 
 using namespace spmvb;
@@ -23,20 +25,22 @@ namespace {
 
 constexpr int CK_WARPS = 8;
 
-// chunk_row[c] = first row r with ptr[r] >= c*CH (c < nchunks); chunk_row[nchunks] = n_rows.
-__global__ void k_chunk_plan(int64_t n_rows, int64_t nnz, int64_t ch, const int32_t* __restrict__ ptr,
-                             int64_t nchunks, int32_t* __restrict__ chunk_row) {
+// chunk_row[c] = first index i of the non-empty row list (the identity when
+// nz_rows is null) whose row starts at or after c*CH; chunk_row[nchunks] = n_nz.
+__global__ void k_chunk_plan(int64_t n_nz, int64_t ch, const int32_t* __restrict__ ptr,
+                             const int32_t* __restrict__ nz_rows, int64_t nchunks, int32_t* __restrict__ chunk_row) {
   for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c <= nchunks;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (c == nchunks) {
-      chunk_row[c] = static_cast<int32_t>(n_rows);
+      chunk_row[c] = static_cast<int32_t>(n_nz);
       continue;
     }
     const int64_t v = c * ch;
-    int64_t lo = 0, hi = n_rows;  // lower_bound over ptr[0..n_rows)
+    int64_t lo = 0, hi = n_nz;
     while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (ptr[mid] < v) lo = mid + 1; else hi = mid;
+      const int64_t mid = (lo + hi) >> 1;
+      const int64_t r = nz_rows ? nz_rows[mid] : mid;
+      if (ptr[r] < v) lo = mid + 1; else hi = mid;
     }
     chunk_row[c] = static_cast<int32_t>(lo);
   }
@@ -52,20 +56,35 @@ struct ChunkSmem {
 template <bool HAS_ELL>
 __device__ __forceinline__ double ell_row(int64_t n_rows, int64_t r, int64_t ell_k, const int32_t* __restrict__ ell_idx,
                                           const double* __restrict__ ell_val, const double* __restrict__ x) {
+  // sequential over the K slots with separately rounded products, as the
+  // reference's spmv_ell (kernels.py:101-104); loads issued 4 slots ahead
   double e = 0.0;
-  if (HAS_ELL)
-    for (int64_t j = 0; j < ell_k; ++j) {
+  if (HAS_ELL) {
+    int64_t j = 0;
+    for (; j + 4 <= ell_k; j += 4) {
+      const int64_t o = j * n_rows + r;
+      const double v0 = ld_stream(ell_val + o), v1 = ld_stream(ell_val + o + n_rows);
+      const double v2 = ld_stream(ell_val + o + 2 * n_rows), v3 = ld_stream(ell_val + o + 3 * n_rows);
+      const int32_t c0 = ld_stream(ell_idx + o), c1 = ld_stream(ell_idx + o + n_rows);
+      const int32_t c2 = ld_stream(ell_idx + o + 2 * n_rows), c3 = ld_stream(ell_idx + o + 3 * n_rows);
+      e = __dadd_rn(e, __dmul_rn(v0, ldx(x, c0)));
+      e = __dadd_rn(e, __dmul_rn(v1, ldx(x, c1)));
+      e = __dadd_rn(e, __dmul_rn(v2, ldx(x, c2)));
+      e = __dadd_rn(e, __dmul_rn(v3, ldx(x, c3)));
+    }
+    for (; j < ell_k; ++j) {
       const int64_t o = j * n_rows + r;
       e = __dadd_rn(e, __dmul_rn(ld_stream(ell_val + o), ldx(x, ld_stream(ell_idx + o))));
     }
+  }
   return e;
 }
 
 template <int S, bool HAS_ELL>
 __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     int64_t n_rows, int64_t nnz, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-    const double* __restrict__ val, const int32_t* __restrict__ chunk_row, int64_t nchunks,
-    int32_t* __restrict__ carry_row, double* __restrict__ carry_val, const double* __restrict__ x,
+    const double* __restrict__ val, const int32_t* __restrict__ nz_rows, const int32_t* __restrict__ chunk_row,
+    int64_t nchunks, int32_t* __restrict__ carry_row, double* __restrict__ carry_val, const double* __restrict__ x,
     double* __restrict__ y, const double* __restrict__ scale_p, int64_t ell_k, const int32_t* __restrict__ ell_idx,
     const double* __restrict__ ell_val) {
   constexpr int CH = 32 * S;
@@ -97,21 +116,15 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     }
   }
   __syncwarp();
-  // 2. rows starting in this chunk
+  // 2. non-empty rows starting in this chunk (at most CH of them)
   const double sc = load_scale(scale_p);
-  const int32_t ra = chunk_row[c], rb = chunk_row[c + 1];
-  for (int64_t r = ra + lane; r < rb; r += 32) {
-    const int32_t s0 = ptr[r], s1 = ptr[r + 1];
-    // HYB: every owned row's ELL part is formed here (lanes on consecutive
-    // rows: coalesced column-major ELL loads); a row with tail entries parks
-    // it unscaled in y[r] for the lane that closes the row's segment.
-    const double e = HAS_ELL ? ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0;
-    if (s1 > s0) {
-      seg[s0 - k0] = static_cast<int32_t>(r);
-      if (HAS_ELL) y[r] = e;
-    } else {
-      y[r] = sc * e;
-    }
+  const int32_t ia = chunk_row[c], ib = chunk_row[c + 1];
+  for (int32_t i = ia + lane; i < ib; i += 32) {
+    const int32_t r = nz_rows ? nz_rows[i] : i;
+    seg[ptr[r] - k0] = r;
+    // HYB: the row's ELL part, parked unscaled in y[r] for the lane that
+    // closes the row's segment
+    if (HAS_ELL) y[r] = ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x);
   }
   __syncwarp();  // also orders the parked y[r] stores before the reads below
   // 3. lane-contiguous segments
@@ -153,10 +166,24 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
   if (lane == 31) right = 0.0;
   if (F) y[open_row] = sc * (HAS_ELL ? y[open_row] + (sum + right) : sum + right);
   if (lane == 0) {
-    // leading entries continue row ra - 1 unless a row starts at position 0
+    // leading entries continue the previous non-empty row unless a row
+    // starts at position 0
     const bool cont = !(fmask & 1u);
-    carry_row[c] = cont ? ra - 1 : -1;
+    carry_row[c] = cont ? (nz_rows ? nz_rows[ia - 1] : ia - 1) : -1;
     carry_val[c] = cont ? rv : 0.0;
+  }
+}
+
+// Empty rows: y = 0, or for HYB the ELL part (rows with an empty tail).
+template <bool HAS_ELL>
+__global__ void k_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, int64_t ell_k,
+                             const int32_t* __restrict__ ell_idx, const double* __restrict__ ell_val,
+                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
+  const double sc = load_scale(scale_p);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!ptr || ld_stream(ptr + r) == ld_stream(ptr + r + 1))  // ptr == NULL: every row is empty
+      y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0;
   }
 }
 
@@ -192,59 +219,56 @@ __global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row
   }
 }
 
-// y = ELL part only (HYB whose tail is empty)
-__global__ void k_ell_only(int64_t n_rows, int64_t ell_k, const int32_t* __restrict__ ell_idx,
-                           const double* __restrict__ ell_val, const double* __restrict__ x, double* __restrict__ y,
-                           const double* __restrict__ scale_p) {
-  const double sc = load_scale(scale_p);
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    y[r] = sc * ell_row<true>(n_rows, r, ell_k, ell_idx, ell_val, x);
-}
-
-template <int S, bool HAS_ELL>
-void launch_chunk_t(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
-                    const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x, double* y,
-                    const double* scale, int64_t ell_k, const int32_t* ell_idx, const double* ell_val,
-                    cudaStream_t s) {
-  constexpr int CH = 32 * S;
-  const int64_t nchunks = (nnz + CH - 1) / CH;
-  const size_t smem = sizeof(ChunkSmem<S>);
-  SPMVB_CUDA(cudaFuncSetAttribute(k_spmv_chunk<S, HAS_ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_spmv_chunk<S, HAS_ELL><<<static_cast<unsigned>((nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem, s>>>(
-      n_rows, nnz, ptr, col, val, chunk_row, nchunks, carry_row, carry_val, x, y, scale, ell_k, ell_idx, ell_val);
-  SPMVB_LAUNCHED("k_spmv_chunk");
-  if (nchunks > 1) {
-    k_chunk_fixup<<<grid_for(nchunks, 256, 148 * 8), 256, 0, s>>>(nchunks, carry_row, carry_val, y, scale);
-    SPMVB_LAUNCHED("k_chunk_fixup");
-  }
-}
-
 int chunk_s() {
   const char* e = getenv("SPMVB_CSR_CHUNK_S");
   return (e && e[0] == '1') ? 16 : 8;  // S = 8 measured faster on C1-C5 (occupancy)
 }
 
-void launch_chunk(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
-                  const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x, double* y,
-                  const double* scale, int64_t ell_k, const int32_t* ell_idx, const double* ell_val, cudaStream_t s) {
-  if (n_rows <= 0) return;
-  if (nnz == 0) {
-    if (ell_k > 0) {
-      k_ell_only<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, ell_k, ell_idx, ell_val, x, y, scale);
-      SPMVB_LAUNCHED("k_ell_only");
-    } else {
-      SPMVB_CUDA(cudaMemsetAsync(y, 0, n_rows * sizeof(double), s));
-    }
-    return;
+struct ChunkArgs {
+  int64_t n_rows, nnz;
+  const int32_t *ptr, *col;
+  const double* val;
+  const int32_t *nz_rows, *chunk_row;
+  int64_t n_nz;
+  int32_t* carry_row;
+  double* carry_val;
+  const double* x;
+  double* y;
+  const double* scale;
+  int64_t ell_k;
+  const int32_t* ell_idx;
+  const double* ell_val;
+};
+
+template <int S, bool HAS_ELL>
+void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
+  constexpr int CH = 32 * S;
+  const int64_t nchunks = (a.nnz + CH - 1) / CH;
+  if (a.n_nz < a.n_rows) {  // empty rows (and, for HYB, rows whose tail is empty)
+    k_empty_rows<HAS_ELL><<<grid_for(a.n_rows, 256, 148 * 32), 256, 0, s>>>(
+        a.n_rows, a.nnz > 0 ? a.ptr : nullptr, a.ell_k, a.ell_idx, a.ell_val, a.x, a.y, a.scale);
+    SPMVB_LAUNCHED("k_empty_rows");
   }
-  const int S = chunk_s();
-  if (ell_k > 0) {
-    if (S == 8) launch_chunk_t<8, true>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, ell_k, ell_idx, ell_val, s);
-    else launch_chunk_t<16, true>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, ell_k, ell_idx, ell_val, s);
+  if (nchunks == 0) return;
+  const size_t smem = sizeof(ChunkSmem<S>);
+  SPMVB_CUDA(cudaFuncSetAttribute(k_spmv_chunk<S, HAS_ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_spmv_chunk<S, HAS_ELL><<<static_cast<unsigned>((nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem, s>>>(
+      a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x, a.y,
+      a.scale, a.ell_k, a.ell_idx, a.ell_val);
+  SPMVB_LAUNCHED("k_spmv_chunk");
+  if (nchunks > 1) {
+    k_chunk_fixup<<<grid_for(nchunks, 256, 148 * 8), 256, 0, s>>>(nchunks, a.carry_row, a.carry_val, a.y, a.scale);
+    SPMVB_LAUNCHED("k_chunk_fixup");
+  }
+}
+
+void launch_chunk(const ChunkArgs& a, cudaStream_t s) {
+  if (a.n_rows <= 0) return;
+  const bool ell = a.ell_k > 0;
+  if (chunk_s() == 16) {
+    if (ell) launch_chunk_t<16, true>(a, s); else launch_chunk_t<16, false>(a, s);
   } else {
-    if (S == 8) launch_chunk_t<8, false>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, 0, nullptr, nullptr, s);
-    else launch_chunk_t<16, false>(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, 0, nullptr, nullptr, s);
+    if (ell) launch_chunk_t<8, true>(a, s); else launch_chunk_t<8, false>(a, s);
   }
 }
 
@@ -257,34 +281,36 @@ extern "C" int64_t spmvb_csr_chunks(int64_t nnz) {
   return nnz > 0 ? (nnz + ch - 1) / ch : 0;
 }
 
-extern "C" int spmvb_csr_chunk_plan(int64_t n_rows, int64_t nnz, const int32_t* ptr, int32_t* chunk_row,
-                                    void* stream) {
+extern "C" int spmvb_csr_chunk_plan(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* nz_rows,
+                                    int64_t n_nz, int32_t* chunk_row, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
+    if (n_rows <= 0) return;
     const int64_t ch = 32 * chunk_s();
     const int64_t nchunks = nnz > 0 ? (nnz + ch - 1) / ch : 0;
-    k_chunk_plan<<<grid_for(nchunks + 1, 256, 148 * 16), 256, 0, s>>>(n_rows, nnz, ch, ptr, nchunks, chunk_row);
+    k_chunk_plan<<<grid_for(nchunks + 1, 256, 148 * 16), 256, 0, s>>>(n_nz, ch, ptr, nz_rows, nchunks, chunk_row);
     SPMVB_LAUNCHED("k_chunk_plan");
   });
 }
 
-extern "C" int spmvb_spmv_csr(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col,
-                                      const double* val, const int32_t* chunk_row, int32_t* carry_row,
-                                      double* carry_val, const double* x, double* y, const double* scale,
-                                      void* stream) {
+extern "C" int spmvb_spmv_csr(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
+                              const int32_t* nz_rows, int64_t n_nz, const int32_t* chunk_row, int32_t* carry_row,
+                              double* carry_val, const double* x, double* y, const double* scale, void* stream) {
   return guard([&] {
-    launch_chunk(n_rows, nnz, ptr, col, val, chunk_row, carry_row, carry_val, x, y, scale, 0, nullptr, nullptr,
+    launch_chunk(ChunkArgs{n_rows, nnz, ptr, col, val, nz_rows, chunk_row, n_nz, carry_row, carry_val, x, y, scale,
+                           0, nullptr, nullptr},
                  as_stream(stream));
   });
 }
 
 extern "C" int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const double* ell_val,
-                                      int64_t tail_nnz, const int32_t* tail_ptr, const int32_t* tail_col,
-                                      const double* tail_val, const int32_t* chunk_row, int32_t* carry_row,
-                                      double* carry_val, const double* x, double* y, const double* scale,
-                                      void* stream) {
+                              int64_t tail_nnz, const int32_t* tail_ptr, const int32_t* tail_col,
+                              const double* tail_val, const int32_t* nz_rows, int64_t n_nz, const int32_t* chunk_row,
+                              int32_t* carry_row, double* carry_val, const double* x, double* y, const double* scale,
+                              void* stream) {
   return guard([&] {
-    launch_chunk(n_rows, tail_nnz, tail_ptr, tail_col, tail_val, chunk_row, carry_row, carry_val, x, y, scale, k,
-                 ell_idx, ell_val, as_stream(stream));
+    launch_chunk(ChunkArgs{n_rows, tail_nnz, tail_ptr, tail_col, tail_val, nz_rows, chunk_row, n_nz, carry_row,
+                           carry_val, x, y, scale, k, ell_idx, ell_val},
+                 as_stream(stream));
   });
 }

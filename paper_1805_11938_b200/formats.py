@@ -92,16 +92,25 @@ class _ChunkPlan:
         self.chunk = int(LIB.spmvb_csr_chunk_size())
         self.chunks = int(LIB.spmvb_csr_chunks(nnz))
         self.chunk_row = _i32(self.chunks + 1, dev)
+        self.nz_rows = None
+        self.n_nz = n_rows
         if n_rows:
             with torch.cuda.device(dev):
-                check(LIB.spmvb_csr_chunk_plan(n_rows, nnz, ptr(ptr_t), ptr(self.chunk_row), _lib.stream(dev)))
+                s = _lib.stream(dev)
+                self.n_nz = _row_stats(ptr_t, n_rows)[2]
+                if self.n_nz < n_rows:
+                    self.nz_rows = _i32(self.n_nz, dev)
+                    if self.n_nz:
+                        check(LIB.spmvb_csr_nonempty_rows(ptr(ptr_t), n_rows, ptr(self.nz_rows), s))
+                check(LIB.spmvb_csr_chunk_plan(n_rows, nnz, ptr(ptr_t), ptr(self.nz_rows), self.n_nz,
+                                               ptr(self.chunk_row), s))
 
     def scratch(self, dev):
         return _i32(max(self.chunks, 1), dev), _f64(max(self.chunks, 1), dev)
 
     @property
     def nbytes(self) -> int:
-        return 4 * (self.chunks + 1)
+        return 4 * (self.chunks + 1) + (4 * self.n_nz if self.nz_rows is not None else 0)
 
 
 class CsrMatrix:

@@ -96,8 +96,8 @@ def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None):
         cr, cv = plan.scratch(m.device)
         check(
             LIB.spmvb_spmv_csr(
-                m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.chunk_row), ptr(cr), ptr(cv),
-                ptr(xd), ptr(y), sp, s,
+                m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.nz_rows), plan.n_nz,
+                ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
             )
         )
 
@@ -155,7 +155,8 @@ def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None):
         check(
             LIB.spmvb_spmv_hyb(
                 m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), t.nnz, ptr(m.tail_ptr), ptr(t.col),
-                ptr(t.data), ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
+                ptr(t.data), ptr(plan.nz_rows), plan.n_nz, ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y),
+                sp, s,
             )
         )
 
