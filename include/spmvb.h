@@ -194,7 +194,7 @@ int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const doub
 
 /* spmv_csr5 (kernels.py:139-174). nonempty_rows may be NULL when every row is
  * non-empty. carry: num_tiles scratch doubles. */
-int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma, const int32_t* tile_ptr,
+int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma, const int32_t* tile_ptr,
                     const uint8_t* bit_flag, const int32_t* col, const double* val, const uint32_t* tile_aux,
                     const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x, double* y,
                     const double* scale, void* stream);

@@ -74,7 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "spmvb_spmv_csr5": (
         c_int,
-        [c_i64, c_i64, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
+        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
     ),
     "spmvb_spmv_ell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp]),
     "spmvb_sell_wide_plan": (c_int, [c_i64, c_i64, vp, vp, P_i64, vp]),

@@ -2,7 +2,6 @@
 #pragma once
 
 #include "prims.cuh"
-#include "tma.cuh"
 
 namespace spmvb {
 

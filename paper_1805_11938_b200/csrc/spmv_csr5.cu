@@ -40,14 +40,14 @@ __device__ __forceinline__ void csr5_emit(const Csr5Ctx& C, double sc, int64_t t
     return;
   }
   const int64_t g = static_cast<int64_t>(aux & 0x7fffffffu) + s;
-  const int64_t r = csr5_row_of(C, g);
-  C.y[r] = sc * v;
-  if (C.nonempty) {
-    const int64_t prev = g > 0 ? csr5_row_of(C, g - 1) : -1;
-    for (int64_t z = prev + 1; z < r; ++z) C.y[z] = 0.0;
-    if (g == C.n_nonempty - 1)
-      for (int64_t z = r + 1; z < C.n_rows; ++z) C.y[z] = 0.0;
-  }
+  C.y[csr5_row_of(C, g)] = sc * v;
+}
+
+// Empty rows never receive a segment: one coalesced pass writes their zeros.
+__global__ void k_csr5_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, double* __restrict__ y) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (ld_stream(ptr + r) == ld_stream(ptr + r + 1)) y[r] = 0.0;
 }
 
 // Generic: one thread per tile, CSR order recovered from the stored layout.
@@ -218,101 +218,6 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
   if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
 }
 
-// TMA-staged fast path for omega == 32, sigma <= 16: a CTA of 8 warps owns 8
-// consecutive full tiles, which are contiguous in stored order, so three bulk
-// copies (values, columns, flags; L2 evict_first) stage them; products are
-// formed CTA-wide with 16 independent x gathers per thread (L2 evict_last);
-// each warp then runs the column-segmented sum of one tile from shared memory.
-constexpr int C5_TPB = 8;
-constexpr int C5_MAX_ENTRIES = C5_TPB * 32 * 16;
-
-struct Csr5TmaSmem {
-  double vals[C5_MAX_ENTRIES];
-  int32_t cols[C5_MAX_ENTRIES];
-  uint8_t flags[C5_MAX_ENTRIES];
-  uint64_t bar;
-};
-
-__global__ void __launch_bounds__(256) k_csr5_tma(Csr5Ctx C, int64_t full_tiles) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Csr5TmaSmem& sm = *reinterpret_cast<Csr5TmaSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int sigma = C.sigma;
-  const int tile = 32 * sigma;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * C5_TPB;
-  const int ntile = full_tiles - t0 < C5_TPB ? static_cast<int>(full_tiles - t0) : C5_TPB;
-  const int cnt = ntile * tile;
-  const int64_t e0 = t0 * tile;
-  if (tid == 0) {
-    mbar_init(&sm.bar, 1);
-    const uint64_t pol = policy_evict_first();
-    mbar_arrive_expect_tx(&sm.bar, static_cast<uint32_t>(cnt) * 13u);
-    bulk_g2s(sm.vals, C.val + e0, cnt * 8u, &sm.bar, pol);
-    bulk_g2s(sm.cols, C.col + e0, cnt * 4u, &sm.bar, pol);
-    bulk_g2s(sm.flags, C.bit_flag + e0, static_cast<uint32_t>(cnt), &sm.bar, pol);
-  }
-  __syncthreads();
-  mbar_wait(&sm.bar, 0);
-  {
-    const uint64_t pol_x = policy_evict_last();
-    constexpr int PER = C5_MAX_ENTRIES / 256;
-    double p[PER];
-#pragma unroll
-    for (int it = 0; it < PER; ++it) {
-      const int e = tid + it * 256;
-      p[it] = e < cnt ? ld_hint(C.x + sm.cols[e], pol_x) : 0.0;
-    }
-#pragma unroll
-    for (int it = 0; it < PER; ++it) {
-      const int e = tid + it * 256;
-      if (e < cnt) sm.vals[e] *= p[it];
-    }
-  }
-  __syncthreads();
-  if (warp >= ntile) return;  // whole warps only: shuffles below stay full-mask
-  const int64_t t = t0 + warp;
-  const uint32_t aux = C.aux[t];
-  const double sc = load_scale(C.scale_p);
-  const int base = warp * tile;
-  int nflags = 0;
-  for (int i = 0; i < sigma; ++i) nflags += sm.flags[base + i * 32 + lane] ? 1 : 0;
-  int incl = nflags;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    int o = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += o;
-  }
-  const int seg_base = incl - nflags;
-  double head = 0.0, sum = 0.0;
-  int seen = 0;
-  for (int i = 0; i < sigma; ++i) {
-    const int idx = base + i * 32 + lane;
-    if (sm.flags[idx]) {
-      if (seen == 0) head = sum;
-      else csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum);
-      ++seen;
-      sum = 0.0;
-    }
-    sum += sm.vals[idx];
-  }
-  const bool F = seen > 0;
-  if (!F) head = sum;
-  double rv = head;
-  bool stop = F;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    double ov = __shfl_down_sync(0xffffffffu, rv, d);
-    bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d) != 0;
-    if (!stop && lane + d < 32) {
-      rv += ov;
-      stop = ostop;
-    }
-  }
-  double right = __shfl_down_sync(0xffffffffu, rv, 1);
-  if (lane == 31) right = 0.0;
-  if (F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
-}
-
 __global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ aux,
                              const double* __restrict__ carry, double* __restrict__ y) {
   // chains of continuation tiles, folded warp-cooperatively as in k_merge_fixup
@@ -346,10 +251,10 @@ __global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile
 
 }  // namespace
 
-extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma, const int32_t* tile_ptr,
-                               const uint8_t* bit_flag, const int32_t* col, const double* val, const uint32_t* tile_aux,
-                               const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x,
-                               double* y, const double* scale, void* stream) {
+extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                               const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col, const double* val,
+                               const uint32_t* tile_aux, const int32_t* nonempty_rows, int64_t n_nonempty,
+                               double* carry, const double* x, double* y, const double* scale, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
@@ -358,6 +263,10 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma
       return;
     }
     if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
+    if (nonempty_rows) {
+      k_csr5_empty_rows<<<grid_for(n_rows, 256, 148 * 32), 256, 0, s>>>(n_rows, ptr, y);
+      SPMVB_LAUNCHED("k_csr5_empty_rows");
+    }
     Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
               nonempty_rows, carry, x, y, scale};
     const int64_t tile = static_cast<int64_t>(omega) * sigma;
@@ -370,11 +279,6 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma
       SPMVB_LAUNCHED("k_csr5_warp");
       generic_begin = full;
     };
-    const bool tma_ok = omega == 32 && sigma <= 16 && aligned16(val) && aligned16(col) && aligned16(bit_flag);
-    // Kernel variant (experiments): SPMVB_CSR5_KERNEL=tma selects the
-    // TMA-staged kernel; the default is the register-unrolled warp kernel.
-    const char* variant = getenv("SPMVB_CSR5_KERNEL");
-    const bool want_tma = variant && variant[0] == 't';
     auto warp_s_launch = [&](auto kern, auto kern_partial, int W) {  // full tiles, then the partial one
       if (full > 0) {
         kern<<<grid_for(full * W, 256), 256, 0, s>>>(C, 0, full);
@@ -386,7 +290,7 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma
       }
       generic_begin = num_tiles;
     };
-    if (!want_tma && (sigma == 16 || sigma == 8) &&
+    if ((sigma == 16 || sigma == 8) &&
         (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
       if (sigma == 16) {
         switch (omega) {
@@ -403,12 +307,6 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, int omega, int sigma
           default: warp_s_launch(k_csr5_warp_s<4, 8, false>, k_csr5_warp_s<4, 8, true>, 4); break;
         }
       }
-    } else if (want_tma && tma_ok && full > 0) {
-      const size_t smem = sizeof(Csr5TmaSmem);
-      SPMVB_CUDA(cudaFuncSetAttribute(k_csr5_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_csr5_tma<<<static_cast<unsigned>((full + C5_TPB - 1) / C5_TPB), 256, smem, s>>>(C, full);
-      SPMVB_LAUNCHED("k_csr5_tma");
-      generic_begin = full;
     } else if (sigma <= 1024 && full > 0) {
       switch (omega) {
         case 32: warp_launch(k_csr5_warp<32>, 32); break;

@@ -111,7 +111,8 @@ def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None):
         carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
         check(
             LIB.spmvb_spmv_csr5(
-                m.n_rows, m.nnz, m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag), ptr(m.indices), ptr(m.data),
+                m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag), ptr(m.indices),
+                ptr(m.data),
                 ptr(m.tile_aux), ptr(m.nonempty_rows), m.n_nonempty, ptr(carry), ptr(xd), ptr(y), sp, s,
             )
         )
