@@ -3,14 +3,15 @@
 // (kernels.py:177-199 spmv_hyb: ELL part + COO tail reduced through the
 // tail's row pointer).
 //
-// A warp owns a chunk of CH = 32*S consecutive nonzeros:
-//  1. coalesced (lane-striped) loads of S column/value pairs per lane, S
-//     independent x gathers in flight per lane, products into shared memory;
+// A warp owns a chunk of CH = 32*S (S = 8) consecutive nonzeros:
+//  1. lane l loads its S consecutive entries with 256-bit loads (one for the
+//     column indices, two for the values: whole sectors, no transposition —
+//     on sm_100 the LDG.256 path makes CSR5's stored reordering unnecessary)
+//     and keeps S independent x gathers in flight;
 //  2. the non-empty rows whose first entry lies in the chunk (a contiguous
 //     range of the non-empty row list, from the analysis step) mark their
-//     start positions with their row id;
-//  3. each lane takes S consecutive products (a CSR5-like column of the
-//     chunk) and sums segments; a warp-shuffle suffix scan joins segments
+//     start positions (bit mask + row id in shared memory);
+//  3. each lane sums its segments; a warp-shuffle suffix scan joins segments
 //     that cross lanes; segment sums are written to y.
 // Entries before the chunk's first row start continue the previous
 // non-empty row: their sum is the chunk's carry, folded by k_chunk_fixup in
@@ -49,8 +50,8 @@ __global__ void k_chunk_plan(int64_t n_nz, int64_t ch, const int32_t* __restrict
 template <int S>
 struct ChunkSmem {
   static constexpr int CH = 32 * S;
-  double prod[CK_WARPS][CH + CH / S];  // skewed: entry e at e + e / S (conflict-free both ways)
-  int32_t seg[CK_WARPS][CH];           // row id of a row starting at position e, else -1
+  int32_t seg[CK_WARPS][CH];          // row id of the row starting at position e (valid where flagged)
+  uint32_t flag[CK_WARPS][CH / 32];   // bit e: a row starts at chunk position e
 };
 
 template <bool HAS_ELL>
@@ -80,13 +81,14 @@ __device__ __forceinline__ double ell_row(int64_t n_rows, int64_t r, int64_t ell
   return e;
 }
 
-template <int S, bool HAS_ELL>
+template <int S, bool HAS_ELL, bool VEC>
 __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     int64_t n_rows, int64_t nnz, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
     const double* __restrict__ val, const int32_t* __restrict__ nz_rows, const int32_t* __restrict__ chunk_row,
     int64_t nchunks, int32_t* __restrict__ carry_row, double* __restrict__ carry_val, const double* __restrict__ x,
     double* __restrict__ y, const double* __restrict__ scale_p, int64_t ell_k, const int32_t* __restrict__ ell_idx,
     const double* __restrict__ ell_val) {
+  static_assert(S == 8, "lane-contiguous loads assume 8 entries (32 B of indices) per lane");
   constexpr int CH = 32 * S;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem<S>& sm = *reinterpret_cast<ChunkSmem<S>*>(smem_raw);
@@ -95,47 +97,49 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
   if (c >= nchunks) return;  // whole warps only
   const int64_t k0 = c * CH;
   const int cnt = static_cast<int>(nnz - k0 < CH ? nnz - k0 : CH);
-  double* prod = sm.prod[w];
   int32_t* seg = sm.seg[w];
+  uint32_t* flag = sm.flag[w];
 
-  // 1. products, lane-striped (coalesced) with S gathers in flight per lane
+  // 1. lane l owns entries [8l, 8l+8): one 256-bit load of its column
+  //    indices and two of its values (full sectors; with the lanes' rows
+  //    consecutive, the x gathers of one instruction fall in few lines on
+  //    banded/stencil matrices), then 8 independent gathers in flight.
+  double v[S];
   {
+    const int e0 = lane * S;
     int32_t ci[S];
-    double vi[S];
+    if (VEC && e0 + S <= cnt) {
+      ld_stream8(col + k0 + e0, ci);
+      ld_stream4(val + k0 + e0, v);
+      ld_stream4(val + k0 + e0 + 4, v + 4);
+    } else {
 #pragma unroll
-    for (int i = 0; i < S; ++i) {
-      const int e = i * 32 + lane;
-      ci[i] = e < cnt ? ld_stream(col + k0 + e) : 0;
-      vi[i] = e < cnt ? ld_stream(val + k0 + e) : 0.0;
+      for (int i = 0; i < S; ++i) {
+        const bool ok = e0 + i < cnt;
+        ci[i] = ok ? ld_stream(col + k0 + e0 + i) : 0;
+        v[i] = ok ? ld_stream(val + k0 + e0 + i) : 0.0;
+      }
     }
 #pragma unroll
-    for (int i = 0; i < S; ++i) {
-      const int e = i * 32 + lane;
-      prod[e + e / S] = e < cnt ? vi[i] * ldx(x, ci[i]) : 0.0;
-      seg[e] = -1;
-    }
+    for (int i = 0; i < S; ++i) v[i] = e0 + i < cnt ? v[i] * ldx(x, ci[i]) : 0.0;
   }
+  if (lane < CH / 32) flag[lane] = 0u;
   __syncwarp();
   // 2. non-empty rows starting in this chunk (at most CH of them)
   const double sc = load_scale(scale_p);
   const int32_t ia = chunk_row[c], ib = chunk_row[c + 1];
   for (int32_t i = ia + lane; i < ib; i += 32) {
     const int32_t r = nz_rows ? nz_rows[i] : i;
-    seg[ptr[r] - k0] = r;
+    const int p = static_cast<int>(ptr[r] - k0);
+    seg[p] = r;
+    atomicOr(&flag[p >> 5], 1u << (p & 31));
     // HYB: the row's ELL part, parked unscaled in y[r] for the lane that
     // closes the row's segment
     if (HAS_ELL) y[r] = ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x);
   }
   __syncwarp();  // also orders the parked y[r] stores before the reads below
   // 3. lane-contiguous segments
-  uint32_t fmask = 0;
-  double v[S];
-#pragma unroll
-  for (int i = 0; i < S; ++i) {
-    const int e = lane * S + i;
-    v[i] = prod[e + e / S];
-    fmask |= (seg[e] >= 0 ? 1u : 0u) << i;
-  }
+  const uint32_t fmask = (flag[lane >> 2] >> ((lane & 3) * S)) & 0xffu;
   double head = 0.0, sum = 0.0;
   int open_row = -1;
 #pragma unroll
@@ -219,10 +223,8 @@ __global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row
   }
 }
 
-int chunk_s() {
-  const char* e = getenv("SPMVB_CSR_CHUNK_S");
-  return (e && e[0] == '1') ? 16 : 8;  // S = 8 measured faster on C1-C5 (occupancy)
-}
+constexpr int CHUNK_S = 8;  // entries per lane: one 256-bit load of indices
+inline int chunk_s() { return CHUNK_S; }
 
 struct ChunkArgs {
   int64_t n_rows, nnz;
@@ -240,6 +242,15 @@ struct ChunkArgs {
   const double* ell_val;
 };
 
+template <int S, bool HAS_ELL, bool VEC>
+void launch_main(const ChunkArgs& a, int64_t nchunks, cudaStream_t s) {
+  const size_t smem = sizeof(ChunkSmem<S>);
+  k_spmv_chunk<S, HAS_ELL, VEC><<<static_cast<unsigned>((nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem,
+                                  s>>>(a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks,
+                                       a.carry_row, a.carry_val, a.x, a.y, a.scale, a.ell_k, a.ell_idx, a.ell_val);
+  SPMVB_LAUNCHED("k_spmv_chunk");
+}
+
 template <int S, bool HAS_ELL>
 void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
   constexpr int CH = 32 * S;
@@ -250,12 +261,9 @@ void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
     SPMVB_LAUNCHED("k_empty_rows");
   }
   if (nchunks == 0) return;
-  const size_t smem = sizeof(ChunkSmem<S>);
-  SPMVB_CUDA(cudaFuncSetAttribute(k_spmv_chunk<S, HAS_ELL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_spmv_chunk<S, HAS_ELL><<<static_cast<unsigned>((nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem, s>>>(
-      a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x, a.y,
-      a.scale, a.ell_k, a.ell_idx, a.ell_val);
-  SPMVB_LAUNCHED("k_spmv_chunk");
+  // 256-bit loads need 32-byte aligned index/value arrays (torch allocations are)
+  if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, s);
+  else launch_main<S, HAS_ELL, false>(a, nchunks, s);
   if (nchunks > 1) {
     k_chunk_fixup<<<grid_for(nchunks, 256, 148 * 8), 256, 0, s>>>(nchunks, a.carry_row, a.carry_val, a.y, a.scale);
     SPMVB_LAUNCHED("k_chunk_fixup");
@@ -264,12 +272,8 @@ void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
 
 void launch_chunk(const ChunkArgs& a, cudaStream_t s) {
   if (a.n_rows <= 0) return;
-  const bool ell = a.ell_k > 0;
-  if (chunk_s() == 16) {
-    if (ell) launch_chunk_t<16, true>(a, s); else launch_chunk_t<16, false>(a, s);
-  } else {
-    if (ell) launch_chunk_t<8, true>(a, s); else launch_chunk_t<8, false>(a, s);
-  }
+  if (a.ell_k > 0) launch_chunk_t<CHUNK_S, true>(a, s);
+  else launch_chunk_t<CHUNK_S, false>(a, s);
 }
 
 }  // namespace
