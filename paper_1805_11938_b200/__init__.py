@@ -51,7 +51,15 @@ from .formats import (  # noqa: E402
     to_sell,
 )
 from . import synth  # noqa: E402
-from .harness import bandwidth_estimate, spmv_bytes, spmv_flops  # noqa: E402
+from .harness import (  # noqa: E402
+    BenchConfig,
+    BenchRecord,
+    bandwidth_estimate,
+    best_labels,
+    run_bench,
+    spmv_bytes,
+    spmv_flops,
+)
 from .kernels import spmv, spmv_csr, spmv_csr5, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
 from .model import DecisionTreeModel, ModelIOError, load_model, predict, select_format  # noqa: E402
 
