@@ -72,6 +72,17 @@ int spmvb_canonicalize_finish(spmvb_canon* plan, int32_t* row_out, int32_t* col_
                               void* stream);
 void spmvb_canonicalize_free(spmvb_canon* plan);
 
+/* read_matrix_market entry tokenizer (coo.py:222-262), host code,
+ * multithreaded: `text` is everything after the size line.  Writes the
+ * expanded 0-based triplets (symmetric off-diagonal entries mirrored,
+ * pattern entries 1.0) into host arrays of capacity `cap` and *n_out.
+ * Returns 0 on success; any nonzero value means "not handled here" (an entry
+ * error or text outside the fast path's ASCII/"\n" grammar) and the caller
+ * re-parses with the reference-semantics parser for the exact error. */
+int spmvb_mm_parse(const char* text, int64_t len, int pattern, int symmetric, int64_t n_rows, int64_t n_cols,
+                   int64_t declared, int64_t cap, int64_t* row_out, int64_t* col_out, double* val_out, int64_t* n_out,
+                   int64_t* err_line, int64_t* err_ij, int n_threads);
+
 /* row_nnz_histogram (coo.py:144-146) on canonical (row-sorted) COO. */
 int spmvb_row_nnz_histogram(const int32_t* row, int64_t nnz, int64_t n_rows, int64_t* counts_out,
                             void* stream);

@@ -8,13 +8,15 @@ compare equal element by element.
 
 ``canonicalize`` runs entirely on the device (LSD radix sort of the
 (row, col) key, numpy-order duplicate sums, zero drop); see
-csrc/coo.cu.  Matrix Market text is parsed on the host (this is not part of
-the data-parallel path) and handed to the GPU ``canonicalize``.
+csrc/coo.cu.  Matrix Market entries are tokenized on the host by a native
+multithreaded parser (csrc/mmio.cpp) and handed to the GPU ``canonicalize``.
 """
 
 from __future__ import annotations
 
 import ctypes
+import os
+import re
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -243,15 +245,6 @@ def dense_spmv_oracle(a: CooMatrix, x):
 # ---------------------------------------------------------------------------
 # Matrix Market I/O (host side; semantics of coo.py:149-278)
 # ---------------------------------------------------------------------------
-def _read_text(source) -> str:
-    if hasattr(source, "read"):
-        raw = source.read()
-        return raw.decode("utf-8") if isinstance(raw, bytes) else raw
-    if isinstance(source, bytes):
-        return source.decode("utf-8")
-    return Path(source).read_text()
-
-
 def _parse_header(lines: list[str]) -> tuple[bool, bool]:
     if not lines:
         raise MatrixMarketError("empty input (line 1)")
@@ -272,13 +265,100 @@ def _parse_header(lines: list[str]) -> tuple[bool, bool]:
     return field == "pattern", symmetry == "symmetric"
 
 
+# bytes on which str.splitlines()/strip() would differ from splitting on "\n"
+_UNUSUAL = re.compile(rb"\r(?!\n)|[\x0b\x0c\x1c-\x1e\x80-\xff]")
+
+
+def _read_bytes(source) -> bytes:
+    if hasattr(source, "read"):
+        raw = source.read()
+        return raw if isinstance(raw, bytes) else raw.encode("utf-8")
+    if isinstance(source, bytes):
+        return source
+    return Path(source).read_bytes()
+
+
+def _fast_triplets(raw: bytes):
+    """Header in Python, entries in the native multithreaded tokenizer
+    (csrc/mmio.cpp).  Returns None whenever the reference-semantics parser
+    must decide (errors, unusual text), so results and messages are the
+    reference's in every case."""
+    nl = raw.find(b"\n")
+    if nl < 0:
+        return None
+    banner = raw[:nl - 1] if raw[:nl].endswith(b"\r") else raw[:nl]
+    if b"\r" in banner:
+        return None
+    try:
+        pattern, symmetric = _parse_header([banner.decode("ascii")])
+    except (MatrixMarketError, UnicodeDecodeError):
+        return None
+    pos = nl + 1
+    size_text = None
+    while pos < len(raw):
+        end = raw.find(b"\n", pos)
+        end = len(raw) if end < 0 else end
+        line = raw[pos:end]
+        pos = end + 1
+        try:
+            cand = line.decode("ascii").strip()
+        except UnicodeDecodeError:
+            return None
+        if cand and not cand.startswith("%"):
+            size_text = cand
+            break
+    if size_text is None or _UNUSUAL.search(raw, 0, pos):
+        return None
+    fields = size_text.split()
+    try:
+        if len(fields) != 3:
+            return None
+        n_rows, n_cols, declared = (int(f) for f in fields)
+    except ValueError:
+        return None
+    if min(n_rows, n_cols, declared) < 0 or max(n_rows, n_cols, declared) > INDEX_LIMIT:
+        return None
+    tail = raw[pos:] if pos <= len(raw) else b""
+    per = 2 if symmetric else 1
+    cap = per * min(declared, tail.count(b"\n") + 1)
+    rows = np.empty(cap, dtype=np.int64)
+    cols = np.empty(cap, dtype=np.int64)
+    vals = np.empty(cap, dtype=np.float64)
+    n_out = ctypes.c_int64()
+    err_line = ctypes.c_int64()
+    err_ij = (ctypes.c_int64 * 2)()
+    status = LIB.spmvb_mm_parse(
+        tail, len(tail), int(pattern), int(symmetric), n_rows, n_cols, declared, cap, rows.ctypes.data,
+        cols.ctypes.data, vals.ctypes.data, ctypes.byref(n_out), ctypes.byref(err_line), err_ij, os.cpu_count() or 1,
+    )
+    if status != 0:
+        return None
+    n = int(n_out.value)
+    return rows[:n], cols[:n], vals[:n], n_rows, n_cols
+
+
 def read_matrix_market(source, *, device=None) -> CooMatrix:
     """Parse coordinate Matrix Market text and canonicalize it on the GPU.
 
     1-based -> 0-based, symmetric storage mirrored, pattern entries = 1.0,
-    errors name the line (MatrixMarketError), as coo.py:158-263.
+    errors name the line (MatrixMarketError), as coo.py:158-263.  Entries are
+    tokenized by the native multithreaded parser; any error or unusual text
+    is re-parsed by the reference-semantics parser below for the exact
+    message.
     """
-    lines = _read_text(source).splitlines()
+    raw = _read_bytes(source)
+    fast = _fast_triplets(raw)
+    if fast is not None:
+        rows, cols, vals, n_rows, n_cols = fast
+        return canonicalize(rows, cols, vals, n_rows, n_cols, device=device)
+    rows, cols, vals, n_rows, n_cols = _parse_text_triplets(raw.decode("utf-8"))
+    return canonicalize(rows, cols, vals, n_rows, n_cols, device=device)
+
+
+def _parse_text_triplets(text: str):
+    """Reference-semantics parser (coo.py:166-262): expanded triplets, or
+    MatrixMarketError naming the offending line."""
+    lines = text.splitlines()
     pattern, symmetric = _parse_header(lines)
     k = 1
     size_text = None
@@ -340,7 +420,7 @@ def read_matrix_market(source, *, device=None) -> CooMatrix:
         raise MatrixMarketError(
             f"entry count mismatch: declared {declared}, found {seen} (line {len(lines)})"
         )
-    return canonicalize(rows, cols, vals, n_rows, n_cols, device=device)
+    return rows, cols, vals, n_rows, n_cols
 
 
 def write_matrix_market(a, dest) -> None:
