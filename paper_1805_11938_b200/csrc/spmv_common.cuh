@@ -16,6 +16,22 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Calls f(r) for every empty row r (ptr[r] == ptr[r+1]) in grid-stride
+// order; each ptr entry is loaded once (ptr[r+1] comes from the next lane).
+template <typename F>
+__device__ __forceinline__ void for_each_empty_row(int64_t n_rows, const int32_t* __restrict__ ptr, F f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31); base < n_rows;
+       base += stride) {  // warp-uniform trip count (shuffles below)
+    const int64_t r = base + lane;
+    const int32_t p0 = r <= n_rows ? ld_stream(ptr + r) : 0;
+    int32_t p1 = __shfl_down_sync(0xffffffffu, p0, 1);
+    if (lane == 31) p1 = r + 1 <= n_rows ? ld_stream(ptr + r + 1) : 0;
+    if (r < n_rows && p0 == p1) f(r);
+  }
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 

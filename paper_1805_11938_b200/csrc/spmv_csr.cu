@@ -184,10 +184,13 @@ __global__ void k_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, in
                              const int32_t* __restrict__ ell_idx, const double* __restrict__ ell_val,
                              const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
   const double sc = load_scale(scale_p);
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (!ptr || ld_stream(ptr + r) == ld_stream(ptr + r + 1))  // ptr == NULL: every row is empty
-      y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0;
+  auto write = [&](int64_t r) { y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0; };
+  if (ptr) {
+    for_each_empty_row(n_rows, ptr, write);
+  } else {  // every row is empty (e.g. a HYB whose tail is empty)
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      write(r);
   }
 }
 
@@ -199,11 +202,19 @@ __global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  auto key_of = [&](int64_t t) -> int32_t { return (t >= 0 && t < num) ? carry_row[t] : -1; };
+  const double sc = load_scale(scale_p);
   for (int64_t w0 = warp_id * 32; w0 < num; w0 += nwarps * 32) {
     const int64_t cc = w0 + lane;
-    const int32_t r = cc < num ? carry_row[cc] : -1;
-    const bool start = r >= 0 && !(cc > 0 && carry_row[cc - 1] == r);
-    unsigned starts = __ballot_sync(0xffffffffu, start);
+    const int32_t r = key_of(cc);
+    int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
+    int32_t rn = __shfl_down_sync(0xffffffffu, r, 1);
+    if (lane == 0) rp = key_of(cc - 1);
+    if (lane == 31) rn = key_of(cc + 1);
+    const bool start = r >= 0 && rp != r;
+    const bool single = start && rn != r;  // a one-chunk chain: folded by its own lane
+    if (single) y[r] += sc * carry_val[cc];
+    unsigned starts = __ballot_sync(0xffffffffu, start && !single);
     while (starts) {
       const int l = __ffs(starts) - 1;
       starts &= starts - 1;
@@ -211,14 +222,14 @@ __global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row
       double acc = 0.0;
       for (int64_t b = w0 + l;; b += 32) {
         const int64_t t = b + lane;
-        const bool in = t < num && carry_row[t] == key;
+        const bool in = key_of(t) == key;
         const unsigned m = __ballot_sync(0xffffffffu, in);
         const int len = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
         if (lane < len) acc += carry_val[t];
         if (len < 32) break;
       }
       acc = warp_sum(acc);
-      if (lane == 0) y[key] += load_scale(scale_p) * acc;
+      if (lane == 0) y[key] += sc * acc;
     }
   }
 }

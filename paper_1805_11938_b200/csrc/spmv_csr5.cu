@@ -45,9 +45,7 @@ __device__ __forceinline__ void csr5_emit(const Csr5Ctx& C, double sc, int64_t t
 
 // Empty rows never receive a segment: one coalesced pass writes their zeros.
 __global__ void k_csr5_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, double* __restrict__ y) {
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    if (ld_stream(ptr + r) == ld_stream(ptr + r + 1)) y[r] = 0.0;
+  for_each_empty_row(n_rows, ptr, [&](int64_t r) { y[r] = 0.0; });
 }
 
 // Generic: one thread per tile, CSR order recovered from the stored layout.
@@ -220,16 +218,26 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
 
 __global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ aux,
                              const double* __restrict__ carry, double* __restrict__ y) {
-  // chains of continuation tiles, folded warp-cooperatively as in k_merge_fixup
+  // Chains of continuation tiles (consecutive tiles whose head continues the
+  // same row).  A chain of one tile — the common case — is folded by its own
+  // lane; longer chains are folded warp-cooperatively 32 tiles per step.
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  auto key_of = [&](int64_t t) -> int32_t {  // continued row of tile t, or -1
+    return (t >= 0 && t < num_tiles && (aux[t] & 0x80000000u)) ? tile_ptr[t] : -1;
+  };
   for (int64_t w0 = warp_id * 32; w0 < num_tiles; w0 += nwarps * 32) {
     const int64_t t = w0 + lane;
-    const bool cont = t < num_tiles && (aux[t] & 0x80000000u);
-    const int32_t r = cont ? tile_ptr[t] : -1;
-    const bool start = cont && !(t > 0 && (aux[t - 1] & 0x80000000u) && tile_ptr[t - 1] == r);
-    unsigned starts = __ballot_sync(0xffffffffu, start);
+    const int32_t r = key_of(t);
+    int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
+    int32_t rn = __shfl_down_sync(0xffffffffu, r, 1);
+    if (lane == 0) rp = key_of(t - 1);
+    if (lane == 31) rn = key_of(t + 1);
+    const bool start = r >= 0 && rp != r;
+    const bool single = start && rn != r;
+    if (single) y[r] = y[r] + carry[t];
+    unsigned starts = __ballot_sync(0xffffffffu, start && !single);
     while (starts) {
       const int l = __ffs(starts) - 1;
       starts &= starts - 1;
@@ -237,7 +245,7 @@ __global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile
       double acc = 0.0;
       for (int64_t b = w0 + l;; b += 32) {
         const int64_t tt = b + lane;
-        const bool in = tt < num_tiles && (aux[tt] & 0x80000000u) && tile_ptr[tt] == key;
+        const bool in = key_of(tt) == key;
         const unsigned m = __ballot_sync(0xffffffffu, in);
         const int len = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
         if (lane < len) acc += carry[tt];
