@@ -30,6 +30,9 @@ template <typename I>
 __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__ col, const double* __restrict__ val,
                                 int64_t n, int64_t n_rows, int64_t n_cols, int colbits, uint64_t* __restrict__ keys,
                                 unsigned long long* bad, int* noncanonical) {
+  // flags are reduced per block before touching global memory: unsorted
+  // input would otherwise put one atomic per entry on a single address
+  int nc_any = 0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t r = static_cast<int64_t>(row[i]);
@@ -37,15 +40,16 @@ __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__
     bool oob = r < 0 || r >= n_rows || c < 0 || c >= n_cols;
     uint64_t key = oob ? 0ull : ((static_cast<uint64_t>(r) << colbits) | static_cast<uint64_t>(c));
     keys[i] = key;
-    if (oob) atomicMin(bad, static_cast<unsigned long long>(i));
+    if (oob) atomicMin(bad, static_cast<unsigned long long>(i));  // rare: any out-of-range entry aborts
     bool nc = (val[i] == 0.0);
     if (i > 0 && !oob) {
       int64_t pr = static_cast<int64_t>(row[i - 1]);
       int64_t pc = static_cast<int64_t>(col[i - 1]);
       if (pr > r || (pr == r && pc >= c)) nc = true;
     }
-    if (nc) atomicOr(noncanonical, 1);
+    nc_any |= nc ? 1 : 0;
   }
+  if (__syncthreads_or(nc_any) && threadIdx.x == 0) atomicOr(noncanonical, 1);
 }
 
 __global__ void k_canon_runs(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,

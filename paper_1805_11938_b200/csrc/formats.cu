@@ -216,6 +216,7 @@ __global__ void k_hyb_fill(int64_t n_rows, int64_t k, const int32_t* __restrict_
       ell_val[j * n_rows + r] = real ? val[a + j] : 0.0;
     }
     ell_row_nnz[r] = kept;
+    if (cnt > LONG_ROW) continue;  // tail copied by a whole CTA (spmvb_hyb_fill)
     const int64_t t0 = tail_ptr[r];
     for (int64_t j = kept; j < cnt; ++j) {
       tail_row[t0 + j - kept] = static_cast<int32_t>(r);
@@ -427,5 +428,16 @@ extern "C" int spmvb_hyb_fill(int64_t n_rows, const int32_t* ptr, const int32_t*
     k_hyb_fill<<<grid_for(n_rows, 256, 148 * 64), 256, 0, s>>>(n_rows, k, ptr, col, val, tail_ptr, ell_idx, ell_val,
                                                                ell_row_nnz, tail_row, tail_col, tail_val);
     SPMVB_LAUNCHED("k_hyb_fill");
+    for_long_rows(
+        [=] __device__(int64_t r) { return static_cast<int64_t>(ptr[r + 1] - ptr[r]); }, n_rows,
+        [=] __device__(int64_t r, int64_t first, int64_t stride) {
+          const int64_t a = ptr[r], cnt = ptr[r + 1] - a, t0 = tail_ptr[r] - k;
+          for (int64_t j = k + first; j < cnt; j += stride) {
+            tail_row[t0 + j] = static_cast<int32_t>(r);
+            tail_col[t0 + j] = col[a + j];
+            tail_val[t0 + j] = val[a + j];
+          }
+        },
+        s);
   });
 }

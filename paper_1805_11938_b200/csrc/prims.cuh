@@ -198,6 +198,40 @@ void device_reduce(int64_t n, Load load, Op op, T identity, T* out, cudaStream_t
 }
 
 // ---------------------------------------------------------------------------
+// Long rows.  Thread-per-row loops serialise power-law rows (R-MAT rows reach
+// ~4e5 entries), so per-row copy kernels skip rows longer than LONG_ROW and a
+// second launch gives each of those rows a whole CTA.
+// ---------------------------------------------------------------------------
+constexpr int64_t LONG_ROW = 512;
+
+template <typename F>
+__global__ void k_per_long_row(const int32_t* __restrict__ list, F f) {
+  f(static_cast<int64_t>(list[blockIdx.x]), static_cast<int64_t>(threadIdx.x), static_cast<int64_t>(blockDim.x));
+}
+
+// Runs f(row, first, stride) with one 256-thread CTA for every row whose
+// count(row) > LONG_ROW (ascending row list built by scan compaction).
+template <typename Count, typename F>
+void for_long_rows(Count count, int64_t n, F f, cudaStream_t s) {
+  if (n <= 0) return;
+  DevBuf<int32_t> list(n, s);
+  DevBuf<int32_t> total(1, s);
+  int32_t* lp = list.get();
+  exclusive_scan<int32_t>(
+      n, [=] __device__(int64_t i) { return count(i) > LONG_ROW ? 1 : 0; },
+      [=] __device__(int64_t i, int32_t v) {
+        if (count(i) > LONG_ROW) lp[v] = static_cast<int32_t>(i);
+      },
+      OpSum{}, 0, total.get(), s);
+  int32_t h = 0;
+  copy_to_host(&h, total.get(), 1, s);
+  if (h > 0) {
+    k_per_long_row<<<static_cast<unsigned>(h), 256, 0, s>>>(lp, f);
+    SPMVB_LAUNCHED("k_per_long_row");
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stable LSD radix sort of (uint64 key, uint32 value) pairs over the low
 // `key_bits` bits.  8-bit digits; each pass = tile histogram, exclusive scan
 // of the digit-major histogram, and a stable tile scatter staged through
