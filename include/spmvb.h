@@ -210,6 +210,26 @@ int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, 
                     const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x, double* y,
                     const double* scale, void* stream);
 
+/* Range plan for spmvb_spmv_csr5_host: n_ranges tile ranges whose first tile
+ * starts a row (no carry chain crosses a range), as HOST int64 arrays of
+ * n_ranges+1 entries: tile_bounds (0 .. num_tiles) and row_bounds (the first
+ * row each range touches; row_bounds[n_ranges] = n_rows).  Synchronizes. */
+int spmvb_csr5_range_bounds(int64_t nnz, int omega, int sigma, const int32_t* tile_ptr, const uint32_t* tile_aux,
+                            int n_ranges, int64_t* tile_bounds, int64_t* row_bounds, void* stream);
+
+/* spmv(tag="csr5", m, x_host) with HOST buffers -- the reference call shape
+ * (kernels.py:139-174, x and y are host numpy arrays there): copies x_host
+ * (n_cols doubles) into x_dev, runs the ranges of the plan above (last to
+ * first) and streams each range's finished rows of y_dev back into y_host on
+ * a second stream while the other ranges compute.  Returns after y_host is complete.
+ * Bit-identical to spmvb_spmv_csr5 on the same inputs.  Pinned host buffers
+ * make the copies asynchronous; pageable ones are still correct. */
+int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                         const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col, const double* val,
+                         const uint32_t* tile_aux, const int32_t* nonempty_rows, int64_t n_nonempty, double* carry,
+                         const double* x_host, double* x_dev, double* y_dev, double* y_host, const double* scale,
+                         int n_ranges, const int64_t* tile_bounds, const int64_t* row_bounds, void* stream);
+
 /* spmv_ell (kernels.py:98-116): per-row sequential accumulation over all k
  * slots (pads included), separately rounded products: bit-identical to the
  * reference kernel. */

@@ -1,6 +1,9 @@
 // CSR5 SpMV (reference kernels.py:139-174 spmv_csr5): per-tile segmented
 // sums over the reference's descriptor layout, warp shuffles across tile
 // columns, and an ordered carry fix-up for rows spanning tiles.
+#include <mutex>
+#include <vector>
+
 #include "spmv_common.cuh"
 
 using namespace spmvb;
@@ -77,12 +80,12 @@ __global__ void k_csr5_generic(Csr5Ctx C, int64_t t_begin, int64_t t_end) {
 // Fast path: W lanes per full tile (omega == W), lane j owns tile column j
 // (sigma consecutive CSR-order entries stored at base + i*W + j).
 template <int W>
-__global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t full_tiles) {
+__global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, int64_t t_end) {
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
-  const int64_t group = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
-  const bool active = group < full_tiles;
-  const int64_t t = active ? group : 0;
+  const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
+  const bool active = group < t_end;
+  const int64_t t = active ? group : t_begin;
   const int sigma = C.sigma;
   const int64_t base = t * static_cast<int64_t>(W) * sigma;
   const uint32_t aux = active ? C.aux[t] : 0u;
@@ -216,18 +219,19 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
   if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
 }
 
-__global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile_ptr, const uint32_t* __restrict__ aux,
-                             const double* __restrict__ carry, double* __restrict__ y) {
+__global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __restrict__ tile_ptr,
+                             const uint32_t* __restrict__ aux, const double* __restrict__ carry, double* __restrict__ y) {
   // Chains of continuation tiles (consecutive tiles whose head continues the
-  // same row).  A chain of one tile — the common case — is folded by its own
-  // lane; longer chains are folded warp-cooperatively 32 tiles per step.
+  // same row) inside [t_begin, t_end).  A chain of one tile — the common
+  // case — is folded by its own lane; longer chains are folded
+  // warp-cooperatively 32 tiles per step, relative to the chain start.
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   auto key_of = [&](int64_t t) -> int32_t {  // continued row of tile t, or -1
-    return (t >= 0 && t < num_tiles && (aux[t] & 0x80000000u)) ? tile_ptr[t] : -1;
+    return (t >= t_begin && t < t_end && (aux[t] & 0x80000000u)) ? tile_ptr[t] : -1;
   };
-  for (int64_t w0 = warp_id * 32; w0 < num_tiles; w0 += nwarps * 32) {
+  for (int64_t w0 = t_begin + warp_id * 32; w0 < t_end; w0 += nwarps * 32) {
     const int64_t t = w0 + lane;
     const int32_t r = key_of(t);
     int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
@@ -257,6 +261,98 @@ __global__ void k_csr5_fixup(int64_t num_tiles, const int32_t* __restrict__ tile
   }
 }
 
+// Tiles [t_begin, t_end) of one SpMV: the per-tile kernel(s), then the carry
+// fix-up of the continuation chains inside the range.  A range that starts at
+// a non-continuation tile folds exactly like the whole matrix would.
+void launch_tiles(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, cudaStream_t s) {
+  if (t_end <= t_begin) return;
+  const int64_t tile = static_cast<int64_t>(C.omega) * C.sigma;
+  const int64_t full = C.nnz / tile;
+  const int64_t fe = t_end < full ? t_end : full;  // full tiles in range: [t_begin, fe)
+  int64_t generic_begin = t_begin;
+  auto warp_launch = [&](auto kern, int W) {
+    if (fe > t_begin) {
+      kern<<<grid_for((fe - t_begin) * W, 256), 256, 0, s>>>(C, t_begin, fe);
+      SPMVB_LAUNCHED("k_csr5_warp");
+      generic_begin = fe;
+    }
+  };
+  auto warp_s_launch = [&](auto kern, auto kern_partial, int W) {  // full tiles, then the partial one
+    if (fe > t_begin) {
+      kern<<<grid_for((fe - t_begin) * W, 256), 256, 0, s>>>(C, t_begin, fe);
+      SPMVB_LAUNCHED("k_csr5_warp_s");
+    }
+    if (t_end > fe && t_end > full) {
+      kern_partial<<<1, 32, 0, s>>>(C, full, t_end);
+      SPMVB_LAUNCHED("k_csr5_warp_s_partial");
+    }
+    generic_begin = t_end;
+  };
+  const int omega = C.omega, sigma = C.sigma;
+  if ((sigma == 16 || sigma == 8) && (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
+    if (sigma == 16) {
+      switch (omega) {
+        case 32: warp_s_launch(k_csr5_warp_s<32, 16, false>, k_csr5_warp_s<32, 16, true>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 16, false>, k_csr5_warp_s<16, 16, true>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 16, false>, k_csr5_warp_s<8, 16, true>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 16, false>, k_csr5_warp_s<4, 16, true>, 4); break;
+      }
+    } else {
+      switch (omega) {
+        case 32: warp_s_launch(k_csr5_warp_s<32, 8, false>, k_csr5_warp_s<32, 8, true>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 8, false>, k_csr5_warp_s<16, 8, true>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 8, false>, k_csr5_warp_s<8, 8, true>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 8, false>, k_csr5_warp_s<4, 8, true>, 4); break;
+      }
+    }
+  } else if (sigma <= 1024) {
+    switch (omega) {
+      case 32: warp_launch(k_csr5_warp<32>, 32); break;
+      case 16: warp_launch(k_csr5_warp<16>, 16); break;
+      case 8: warp_launch(k_csr5_warp<8>, 8); break;
+      case 4: warp_launch(k_csr5_warp<4>, 4); break;
+      case 2: warp_launch(k_csr5_warp<2>, 2); break;
+      default: break;
+    }
+  }
+  if (generic_begin < t_end) {
+    k_csr5_generic<<<grid_for(t_end - generic_begin, 128, 148 * 64), 128, 0, s>>>(C, generic_begin, t_end);
+    SPMVB_LAUNCHED("k_csr5_generic");
+  }
+  if (t_end - t_begin > 1 || t_begin > 0) {
+    k_csr5_fixup<<<grid_for(t_end - t_begin, 256, 148 * 8), 256, 0, s>>>(t_begin, t_end, C.tile_ptr, C.aux, C.carry,
+                                                                         C.y);
+    SPMVB_LAUNCHED("k_csr5_fixup");
+  }
+}
+
+// First tile at or after `target` whose head starts a row (not a continuation).
+__global__ void k_csr5_range_starts(int64_t num_tiles, const uint32_t* __restrict__ aux, int n_ranges,
+                                    int64_t* __restrict__ bounds) {
+  const int k = blockIdx.x + 1;  // interior bounds 1 .. n_ranges-1
+  const int lane = threadIdx.x;
+  const int64_t target = num_tiles * k / n_ranges;
+  int64_t found = num_tiles;
+  for (int64_t b = target; b < num_tiles; b += 32) {
+    const int64_t t = b + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, t < num_tiles && !(aux[t] & 0x80000000u));
+    if (m) {
+      found = b + __ffs(m) - 1;
+      break;
+    }
+  }
+  if (lane == 0) bounds[k] = found;
+}
+
+cudaStream_t copy_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) fail(SPMVB_INVALID_ARG, "device ordinal out of range");
+  if (!streams[dev]) SPMVB_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+  return streams[dev];
+}
+
 }  // namespace
 
 extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
@@ -278,61 +374,99 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, 
     Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
               nonempty_rows, carry, x, y, scale};
     const int64_t tile = static_cast<int64_t>(omega) * sigma;
-    const int64_t num_tiles = (nnz + tile - 1) / tile;
-    const int64_t full = nnz / tile;
-    int64_t generic_begin = 0;
-    auto warp_launch = [&](auto kern, int W) {
-      int64_t threads = full * W;
-      kern<<<grid_for(threads, 256), 256, 0, s>>>(C, full);
-      SPMVB_LAUNCHED("k_csr5_warp");
-      generic_begin = full;
-    };
-    auto warp_s_launch = [&](auto kern, auto kern_partial, int W) {  // full tiles, then the partial one
-      if (full > 0) {
-        kern<<<grid_for(full * W, 256), 256, 0, s>>>(C, 0, full);
-        SPMVB_LAUNCHED("k_csr5_warp_s");
-      }
-      if (num_tiles > full) {
-        kern_partial<<<1, 32, 0, s>>>(C, full, num_tiles);
-        SPMVB_LAUNCHED("k_csr5_warp_s_partial");
-      }
-      generic_begin = num_tiles;
-    };
-    if ((sigma == 16 || sigma == 8) &&
-        (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
-      if (sigma == 16) {
-        switch (omega) {
-          case 32: warp_s_launch(k_csr5_warp_s<32, 16, false>, k_csr5_warp_s<32, 16, true>, 32); break;
-          case 16: warp_s_launch(k_csr5_warp_s<16, 16, false>, k_csr5_warp_s<16, 16, true>, 16); break;
-          case 8: warp_s_launch(k_csr5_warp_s<8, 16, false>, k_csr5_warp_s<8, 16, true>, 8); break;
-          default: warp_s_launch(k_csr5_warp_s<4, 16, false>, k_csr5_warp_s<4, 16, true>, 4); break;
-        }
-      } else {
-        switch (omega) {
-          case 32: warp_s_launch(k_csr5_warp_s<32, 8, false>, k_csr5_warp_s<32, 8, true>, 32); break;
-          case 16: warp_s_launch(k_csr5_warp_s<16, 8, false>, k_csr5_warp_s<16, 8, true>, 16); break;
-          case 8: warp_s_launch(k_csr5_warp_s<8, 8, false>, k_csr5_warp_s<8, 8, true>, 8); break;
-          default: warp_s_launch(k_csr5_warp_s<4, 8, false>, k_csr5_warp_s<4, 8, true>, 4); break;
-        }
-      }
-    } else if (sigma <= 1024 && full > 0) {
-      switch (omega) {
-        case 32: warp_launch(k_csr5_warp<32>, 32); break;
-        case 16: warp_launch(k_csr5_warp<16>, 16); break;
-        case 8: warp_launch(k_csr5_warp<8>, 8); break;
-        case 4: warp_launch(k_csr5_warp<4>, 4); break;
-        case 2: warp_launch(k_csr5_warp<2>, 2); break;
-        default: break;
-      }
-    }
-    if (generic_begin < num_tiles) {
-      k_csr5_generic<<<grid_for(num_tiles - generic_begin, 128, 148 * 64), 128, 0, s>>>(C, generic_begin, num_tiles);
-      SPMVB_LAUNCHED("k_csr5_generic");
-    }
-    if (num_tiles > 1) {
-      k_csr5_fixup<<<grid_for(num_tiles, 256, 148 * 8), 256, 0, s>>>(num_tiles, tile_ptr, tile_aux, carry, y);
-      SPMVB_LAUNCHED("k_csr5_fixup");
-    }
+    launch_tiles(C, 0, (nnz + tile - 1) / tile, s);
   });
 }
 
+
+extern "C" int spmvb_csr5_range_bounds(int64_t nnz, int omega, int sigma, const int32_t* tile_ptr,
+                                       const uint32_t* tile_aux, int n_ranges, int64_t* tile_bounds,
+                                       int64_t* row_bounds, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
+    if (n_ranges < 1) fail(SPMVB_INVALID_ARG, "n_ranges must be >= 1");
+    const int64_t tile = static_cast<int64_t>(omega) * sigma;
+    const int64_t num_tiles = (nnz + tile - 1) / tile;
+    DevBuf<int64_t> d(n_ranges + 1, s);
+    if (n_ranges > 1 && num_tiles > 0) {
+      k_csr5_range_starts<<<n_ranges - 1, 32, 0, s>>>(num_tiles, tile_aux, n_ranges, d.ptr);
+      SPMVB_LAUNCHED("k_csr5_range_starts");
+      SPMVB_CUDA(cudaMemcpyAsync(tile_bounds + 1, d.ptr + 1, (n_ranges - 1) * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<int32_t> tp(num_tiles + 1);
+    SPMVB_CUDA(cudaMemcpyAsync(tp.data(), tile_ptr, (num_tiles + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPMVB_CUDA(cudaStreamSynchronize(s));
+    tile_bounds[0] = 0;
+    tile_bounds[n_ranges] = num_tiles;
+    if (num_tiles == 0)
+      for (int k = 1; k < n_ranges; ++k) tile_bounds[k] = 0;
+    for (int k = 1; k <= n_ranges; ++k)
+      if (tile_bounds[k] < tile_bounds[k - 1]) tile_bounds[k] = tile_bounds[k - 1];
+    for (int k = 0; k <= n_ranges; ++k) row_bounds[k] = tp[tile_bounds[k]];
+    row_bounds[0] = 0;
+  });
+}
+
+extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* ptr, int omega,
+                                    int sigma, const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col,
+                                    const double* val, const uint32_t* tile_aux, const int32_t* nonempty_rows,
+                                    int64_t n_nonempty, double* carry, const double* x_host, double* x_dev,
+                                    double* y_dev, double* y_host, const double* scale, int n_ranges,
+                                    const int64_t* tile_bounds, const int64_t* row_bounds, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
+    if (n_ranges < 1 || !tile_bounds || !row_bounds) fail(SPMVB_INVALID_ARG, "range plan missing");
+    if (n_cols > 0) SPMVB_CUDA(cudaMemcpyAsync(x_dev, x_host, n_cols * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (n_rows <= 0) {
+      SPMVB_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    if (nnz == 0) {
+      SPMVB_CUDA(cudaMemsetAsync(y_dev, 0, n_rows * sizeof(double), s));
+      SPMVB_CUDA(cudaMemcpyAsync(y_host, y_dev, n_rows * sizeof(double), cudaMemcpyDeviceToHost, s));
+      SPMVB_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    const int64_t tile = static_cast<int64_t>(omega) * sigma;
+    const int64_t num_tiles = (nnz + tile - 1) / tile;
+    if (tile_bounds[0] != 0 || tile_bounds[n_ranges] != num_tiles || row_bounds[0] != 0)
+      fail(SPMVB_INVALID_ARG, "range plan does not cover the tiles");
+    int dev = 0;
+    SPMVB_CUDA(cudaGetDevice(&dev));
+    cudaStream_t cs = copy_stream(dev);
+    if (nonempty_rows) {
+      k_csr5_empty_rows<<<grid_for(n_rows, 256, 148 * 32), 256, 0, s>>>(n_rows, ptr, y_dev);
+      SPMVB_LAUNCHED("k_csr5_empty_rows");
+    }
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
+              nonempty_rows, carry, x_dev, y_dev, scale};
+    std::vector<cudaEvent_t> evs;
+    auto event_on = [&](cudaStream_t st) {
+      cudaEvent_t e;
+      SPMVB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      SPMVB_CUDA(cudaEventRecord(e, st));
+      return e;
+    };
+    // Ranges run last-to-first: R-MAT-like matrices put their light rows at
+    // the end, so the first ranges finish many rows and the copy-back starts
+    // early.  No carry chain crosses a range (each starts at a row-start
+    // tile), so the rows of a range are final after its own fix-up.
+    for (int k = n_ranges - 1; k >= 0; --k) {
+      const int64_t tb = tile_bounds[k], te = tile_bounds[k + 1];
+      if (te < tb || te > num_tiles) fail(SPMVB_INVALID_ARG, "range plan is not monotone");
+      launch_tiles(C, tb, te, s);
+      const int64_t lo = row_bounds[k], hi = k + 1 == n_ranges ? n_rows : row_bounds[k + 1];
+      if (hi > lo) {
+        SPMVB_CUDA(cudaStreamWaitEvent(cs, event_on(s), 0));
+        SPMVB_CUDA(cudaMemcpyAsync(y_host + lo, y_dev + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, cs));
+      }
+    }
+    SPMVB_CUDA(cudaStreamWaitEvent(s, event_on(cs), 0));
+    SPMVB_CUDA(cudaStreamSynchronize(s));
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  });
+}

@@ -162,6 +162,7 @@ class Csr5Matrix:
         self.tile_aux = tile_aux
         self.nonempty_rows = nonempty_rows
         self.n_nonempty = int(n_nonempty)
+        self._ranges = {}
 
     @property
     def nnz(self) -> int:
@@ -170,6 +171,22 @@ class Csr5Matrix:
     @property
     def device(self) -> torch.device:
         return self.ptr.device
+
+    def range_plan(self, n_ranges: int) -> tuple[np.ndarray, np.ndarray]:
+        """(tile_bounds, row_bounds) of ``n_ranges`` tile ranges that each start
+        at a row-start tile (spmvb_csr5_range_bounds); cached per count.  The
+        host-buffer SpMV streams each range's finished rows back while the
+        next range computes."""
+        n_ranges = max(1, int(n_ranges))
+        if n_ranges not in self._ranges:
+            tb = np.zeros(n_ranges + 1, dtype=np.int64)
+            rb = np.zeros(n_ranges + 1, dtype=np.int64)
+            with torch.cuda.device(self.device):
+                check(LIB.spmvb_csr5_range_bounds(self.nnz, self.omega, self.sigma, ptr(self.tile_ptr),
+                                                  ptr(self.tile_aux), n_ranges, tb.ctypes.data, rb.ctypes.data,
+                                                  _lib.stream(self.device)))
+            self._ranges[n_ranges] = (tb, rb)
+        return self._ranges[n_ranges]
 
     def __repr__(self) -> str:
         return f"Csr5Matrix({self.n_rows}x{self.n_cols}, nnz={self.nnz}, omega={self.omega}, sigma={self.sigma})"

@@ -79,12 +79,35 @@ def _out(m, out):
     return out
 
 
+def _is_host(a) -> bool:
+    return a is not None and not (isinstance(a, torch.Tensor) and a.is_cuda)
+
+
+def _host_out(out, n_rows: int) -> torch.Tensor:
+    """A host ``out=`` buffer (CPU float64 tensor or writeable numpy array of
+    n_rows elements) as a CPU tensor sharing its memory."""
+    t = out if isinstance(out, torch.Tensor) else None
+    if t is None and isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.writeable:
+        t = torch.from_numpy(out)
+    if t is None or t.dtype != torch.float64 or t.numel() != n_rows or not t.is_contiguous():
+        raise ValueError("out must be a contiguous float64 tensor/array with n_rows elements")
+    return t.reshape(-1)
+
+
 def _run(m, x, out, scale, launch):
+    host = _is_host(out)
+    out_h = _host_out(out, m.n_rows) if host else None
     xd, how = _prepare_x(x, m.n_cols, m.device)
-    y = _out(m, out)
+    y = _out(m, None if host else out)
     if m.n_rows:
         with torch.cuda.device(m.device):
             launch(xd, y, ptr(scale) if scale is not None else None, _lib.stream(m.device))
+    if host:
+        pinned = out_h.is_pinned()
+        out_h.copy_(y, non_blocking=pinned)
+        if pinned:
+            torch.cuda.current_stream(m.device).synchronize()
+        return out
     return _finish_y(y, how)
 
 
@@ -104,8 +127,15 @@ def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None):
     return _run(m, x, out, scale, launch)
 
 
-def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = A x for CSR5: per-tile segmented sums + ordered carry fix-up (kernels.py:139-174)."""
+def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None, ranges: int = 16):
+    """y = A x for CSR5: per-tile segmented sums + ordered carry fix-up (kernels.py:139-174).
+
+    Host x with a host (or no) ``out`` runs the streamed host-buffer entry
+    point: x is copied in once, then ``ranges`` tile ranges compute in order
+    while each range's finished rows of y are copied back on a second stream.
+    """
+    if _is_host(x) and (out is None or _is_host(out)):
+        return _spmv_csr5_host(m, x, out, scale, ranges)
 
     def launch(xd, y, sp, s):
         carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
@@ -118,6 +148,39 @@ def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None):
         )
 
     return _run(m, x, out, scale, launch)
+
+
+def _spmv_csr5_host(m: Csr5Matrix, x, out, scale, ranges: int):
+    if isinstance(x, torch.Tensor):
+        xh = x.reshape(-1)
+        kind = "tensor"
+    else:
+        xh = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64).ravel()))
+        kind = "numpy"
+    if xh.shape[0] != m.n_cols:
+        raise ValueError(f"x has length {xh.shape[0]}, expected {m.n_cols}")
+    xh = xh.to(torch.float64).contiguous()
+    if out is not None:
+        yh = _host_out(out, m.n_rows)
+    else:
+        yh = torch.empty(m.n_rows, dtype=torch.float64, pin_memory=kind == "tensor" and xh.is_pinned())
+    dev = m.device
+    tb, rb = m.range_plan(ranges)
+    xd = torch.empty(max(m.n_cols, 1), dtype=torch.float64, device=dev)
+    yd = torch.empty(max(m.n_rows, 1), dtype=torch.float64, device=dev)
+    carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        check(
+            LIB.spmvb_spmv_csr5_host(
+                m.n_rows, m.n_cols, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag),
+                ptr(m.indices), ptr(m.data), ptr(m.tile_aux), ptr(m.nonempty_rows), m.n_nonempty, ptr(carry),
+                ptr(xh), ptr(xd), ptr(yd), ptr(yh), ptr(scale) if scale is not None else None, len(tb) - 1,
+                tb.ctypes.data, rb.ctypes.data, _lib.stream(dev),
+            )
+        )
+    if out is not None:
+        return out
+    return yh if kind == "tensor" else yh.numpy()
 
 
 def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):

@@ -147,6 +147,40 @@ def test_containers(sp):
     assert yd.is_cuda
 
 
+def test_host_buffers(sp, rng):
+    """Host x / host out= calls: bit-identical to the device call; the CSR5
+    streamed entry point (spmvb_spmv_csr5_host) for every range count,
+    including more ranges than tiles and chains of continuation tiles."""
+    r, c, v = sp.synth.rmat_triplets(scale=13, edge_factor=12, seed=9)
+    a = sp.canonicalize(r, c, v, 1 << 13, 1 << 13)
+    x = rng.uniform(-1.0, 1.0, size=1 << 13)
+    xd = torch.from_numpy(x).cuda()
+    for tag, kw in [("csr", {}), ("csr5", dict(omega=32, sigma=16)), ("csr5", dict(omega=4, sigma=16)),
+                    ("csr5", dict(omega=3, sigma=5)), ("hyb", {}), ("sell", dict(sell_c=32, sell_sigma=64))]:
+        m = sp.convert(tag, a, **kw)
+        yd = np_(sp.spmv(tag, m, xd))
+        assert same_bits(sp.spmv(tag, m, x), yd), tag
+        assert same_bits(sp.spmv(tag, m, torch.from_numpy(x).pin_memory()), yd), tag
+        out = torch.empty(m.n_rows, dtype=torch.float64).pin_memory()
+        assert sp.spmv(tag, m, torch.from_numpy(x).pin_memory(), out=out) is out and same_bits(out, yd), tag
+        outn = np.empty(m.n_rows)
+        assert sp.spmv(tag, m, x, out=outn) is outn and same_bits(outn, yd), tag
+        if tag == "csr5":
+            for k in (1, 2, 3, 8, 64, 10 ** 6):
+                tb, rb = m.range_plan(k)
+                assert tb[0] == 0 and tb[-1] == m.num_tiles and np.all(np.diff(tb) >= 0)
+                assert rb[0] == 0 and rb[-1] == m.n_rows and np.all(np.diff(rb) >= 0)
+                aux = np_(m.tile_aux).view(np.uint32)
+                inner = tb[1:-1][tb[1:-1] < m.num_tiles]
+                assert not np.any(aux[inner] >> 31), k  # ranges start at row-start tiles
+                assert same_bits(sp.spmv_csr5(m, x, ranges=k), yd), (kw, k)
+    with pytest.raises(ValueError, match="out"):
+        sp.spmv("csr", sp.to_csr(a), x, out=np.empty(3))
+    # empty matrix / zero nnz through the host entry point
+    e = sp.to_csr5(sp.canonicalize([], [], [], 5, 4), 4, 16)
+    assert sp.spmv("csr5", e, np.ones(4)).tolist() == [0.0] * 5
+
+
 def test_errors(sp):
     r, c, v = demo_triplets()
     a = sp.canonicalize(r, c, v, 4, 4)
