@@ -272,7 +272,28 @@ def run_ours(args):
     def local_spmv(xv, out, scale):
         sp.spmv(tag, m, xv, out=out, scale=scale)
 
-    pi = spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_full)
+    # overlap (N > 1, CSR5 shards): row-aligned tile ranges, light rows first,
+    # each range's rows sent to the peers while the next range computes
+    ranges, range_fn = None, None
+    if world > 1 and tag == "csr5" and args.overlap_ranges > 1:
+        tb, rb = m.range_plan(args.overlap_ranges)
+        k_all = len(tb) - 1
+        plan = [(int(rb[k]), int(rb[k + 1]) if k + 1 < k_all else m.n_rows, int(tb[k]), int(tb[k + 1]))
+                for k in range(k_all)][::-1]
+        ranges = [(a, b) for a, b, _, _ in plan]
+        carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=dev)
+
+        def range_fn(k, xv, out, scale):
+            a, b, t0, t1 = plan[k]
+            sp.spmv_csr5_tiles(m, xv, out, t0, t1, a, b, scale=scale, carry=carry)
+
+    def make_pi(exchange):
+        return spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_full, exchange=exchange,
+                                     local_cols=shard.indices if exchange == "sparse" else None,
+                                     local_ranges=ranges if exchange == "allgatherv" else None,
+                                     local_spmv_range=range_fn)
+
+    pi = make_pi(args.exchange)
     for _ in range(warmup):
         pi.step()
     torch.cuda.synchronize()
@@ -304,6 +325,30 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_loop = float(tt.item())
     value = 2.0 * nnz * args.steps / t_loop / 1e9
+    exchange = {"mode": pi.exchange, "overlap_ranges": len(ranges) if ranges else 1}
+    if world > 1:
+        # the other exchange, same steps, for comparison (report both)
+        other = "allgatherv" if pi.exchange == "sparse" else "sparse"
+        vol = getattr(pi, "exchange_volume", None)
+        del pi
+        pj = make_pi(other)
+        for _ in range(warmup):
+            pj.step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            pj.step()
+        ev1.record()
+        torch.cuda.synchronize()
+        tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        vol = vol or getattr(pj, "exchange_volume", None)
+        exchange.update({f"ms_per_step_{pj.exchange}": float(tt.item()) / args.steps * 1e3,
+                         f"ms_per_step_{exchange['mode']}": t_loop / args.steps * 1e3})
+        if vol:
+            exchange["rank0_volume_entries"] = vol
+        del pj
 
     # ---- end to end through the public API with host buffers ----
     # (host x in, host y out; the output buffer is the caller's, like numpy's out=)
@@ -347,7 +392,8 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "format": tag, "params": formats[tag]["params"], "n": n,
                        "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
-                       "step": "y=s*A x; ||y||^2 all-reduce; all-gatherv x; s=1/||y||",
+                       "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"
+                                if world > 1 else "y=s*A x; ||y||^2; s=1/||y||"),
                        "l2": "inputs larger than L2 (matrix >= 6 GB), no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -356,6 +402,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "exchange": exchange,
             "clocks": clk,
             "formats": formats,
             "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "to_csr_s": t_csr,
@@ -379,6 +426,11 @@ def main():
     ap.add_argument("--formats", default="csr5")
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--overlap-ranges", type=int, default=4,
+                    help="N > 1, CSR5 shards: row ranges whose all-gatherv overlaps the remaining local SpMV")
+    ap.add_argument("--exchange", choices=["allgatherv", "sparse"], default="allgatherv",
+                    help="x exchange between row blocks (N > 1): the north-star all-gather of x (default), or "
+                         "only the entries each shard reads; the other one is timed too and reported")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)
     ap.add_argument("--cpu-keep-mod", type=int, default=64)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)

@@ -210,6 +210,18 @@ int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, 
                     const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x, double* y,
                     const double* scale, void* stream);
 
+/* One range of spmvb_spmv_csr5: zero the empty rows of [row_begin, row_end)
+ * and run tiles [t_begin, t_end) with their carry fix-up.  With the ranges
+ * of spmvb_csr5_range_bounds (each starting at a row-start tile) the ranges
+ * may run in any order and rows [row_bounds[k], row_bounds[k+1]) are final
+ * after range k -- the multi-GPU power iteration sends them to the peers
+ * while the next range computes.  Bit-identical to spmvb_spmv_csr5. */
+int spmvb_spmv_csr5_tiles(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                          const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col, const double* val,
+                          const uint32_t* tile_aux, const int32_t* nonempty_rows, int64_t n_nonempty, double* carry,
+                          const double* x, double* y, const double* scale, int64_t t_begin, int64_t t_end,
+                          int64_t row_begin, int64_t row_end, void* stream);
+
 /* Range plan for spmvb_spmv_csr5_host: n_ranges tile ranges whose first tile
  * starts a row (no carry chain crosses a range), as HOST int64 arrays of
  * n_ranges+1 entries: tile_bounds (0 .. num_tiles) and row_bounds (the first
@@ -253,6 +265,18 @@ int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int6
 int spmvb_sumsq(const double* y, int64_t n, double* out, void* stream);
 /* scale_out = 1/sqrt(*sumsq) (device scalars). */
 int spmvb_inv_sqrt(const double* sumsq, double* scale_out, void* stream);
+
+/* Sparse x exchange of the row-block power iteration (a shard
+ * reads only ~20% of the columns at C4/C5, so receiving just those entries
+ * cuts the per-step exchange ~4-5x against the full all-gatherv).
+ * spmvb_column_set: sorted distinct column ids of col[0..nnz) into cols_out
+ * (NULL = count only); *n_out (host) = how many.  Synchronizes.
+ * spmvb_gather_f64: dst[i] = src[idx[i] - base] (owner packs requested rows).
+ * spmvb_scatter_f64: dst[idx[i]] = src[i] (receiver unpacks into x). */
+int spmvb_column_set(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cols_out, int64_t* n_out,
+                     void* stream);
+int spmvb_gather_f64(const double* src, int64_t base, const int32_t* idx, int64_t n, double* dst, void* stream);
+int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream);
 
 /* ======================================================================== */
 /* Features — replaces features.py:69-84 (extract_features)                 */

@@ -60,7 +60,7 @@ from .harness import (  # noqa: E402
     spmv_bytes,
     spmv_flops,
 )
-from .kernels import spmv, spmv_csr, spmv_csr5, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
+from .kernels import spmv, spmv_csr, spmv_csr5, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
 from .model import DecisionTreeModel, ModelIOError, load_model, predict, select_format  # noqa: E402
 
 __version__ = "0.1.0"

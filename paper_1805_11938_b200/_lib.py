@@ -81,6 +81,11 @@ SIGNATURES: dict[str, tuple] = {
         [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
     ),
     "spmvb_csr5_range_bounds": (c_int, [c_i64, c_int, c_int, vp, vp, c_int, vp, vp, vp]),
+    "spmvb_spmv_csr5_tiles": (
+        c_int,
+        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, c_i64, c_i64, c_i64, c_i64,
+         vp],
+    ),
     "spmvb_spmv_csr5_host": (
         c_int,
         [c_i64, c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, c_int,
@@ -91,6 +96,9 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp]),
     "spmvb_sumsq": (c_int, [vp, c_i64, vp, vp]),
     "spmvb_inv_sqrt": (c_int, [vp, vp, vp]),
+    "spmvb_column_set": (c_int, [vp, c_i64, c_i64, vp, P_i64, vp]),
+    "spmvb_gather_f64": (c_int, [vp, c_i64, vp, c_i64, vp, vp]),
+    "spmvb_scatter_f64": (c_int, [vp, vp, c_i64, vp, vp]),
     "spmvb_csr_features": (c_int, [c_i64, c_i64, c_i64, vp, P_dbl, vp]),
     "spmvb_csr_extra_features": (c_int, [c_i64, c_i64, vp, vp, P_dbl, vp]),
     "spmvb_rmat_begin": (c_int, [c_int, c_i64, c_dbl, c_dbl, c_dbl, c_u64, P_vp, P_i64, vp]),

@@ -1,0 +1,75 @@
+// Sparse x exchange for the row-block power iteration:
+// each rank receives only the x entries its shard's columns touch, not the
+// whole all-gathered vector.  Setup finds the shard's column set; every step
+// the owner gathers the requested entries of its y block into one send
+// buffer and the receiver scatters them into its x.
+#include "prims.cuh"
+
+using namespace spmvb;
+
+namespace {
+
+__global__ void k_mark_columns(const int32_t* __restrict__ col, int64_t nnz, uint8_t* __restrict__ flags) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    flags[col[k]] = 1;
+}
+
+__global__ void k_gather_f64(const double* __restrict__ src, int64_t base, const int32_t* __restrict__ idx, int64_t n,
+                             double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[idx[i] - base];
+}
+
+__global__ void k_scatter_f64(const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                              double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[idx[i]] = src[i];
+}
+
+}  // namespace
+
+extern "C" int spmvb_column_set(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cols_out, int64_t* n_out,
+                                void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (!n_out) fail(SPMVB_INVALID_ARG, "n_out is required");
+    *n_out = 0;
+    if (n_cols <= 0 || nnz <= 0) return;
+    DevBuf<uint8_t> flags(n_cols, s);
+    const uint8_t* f = flags.get();
+    SPMVB_CUDA(cudaMemsetAsync(flags.get(), 0, n_cols, s));
+    k_mark_columns<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(col, nnz, flags.get());
+    SPMVB_LAUNCHED("k_mark_columns");
+    DevBuf<int64_t> total(1, s);
+    exclusive_scan<int64_t>(
+        n_cols, [=] __device__(int64_t i) -> int64_t { return f[i]; },
+        [=] __device__(int64_t i, int64_t v) {
+          if (cols_out && f[i]) cols_out[v] = static_cast<int32_t>(i);
+        },
+        OpSum{}, int64_t{0}, total.get(), s);
+    SPMVB_CUDA(cudaMemcpyAsync(n_out, total.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPMVB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int spmvb_gather_f64(const double* src, int64_t base, const int32_t* idx, int64_t n, double* dst,
+                                void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n <= 0) return;
+    k_gather_f64<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(src, base, idx, n, dst);
+    SPMVB_LAUNCHED("k_gather_f64");
+  });
+}
+
+extern "C" int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n <= 0) return;
+    k_scatter_f64<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(src, idx, n, dst);
+    SPMVB_LAUNCHED("k_scatter_f64");
+  });
+}

@@ -326,6 +326,19 @@ void launch_tiles(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, cudaStream_t
   }
 }
 
+// One range of a range plan: zero the empty rows of [row_begin, row_end),
+// then tiles [t_begin, t_end) with their fix-up.  Row-aligned ranges (each
+// starting at a row-start tile) may run in any order.
+void launch_range(const Csr5Ctx& C, const int32_t* ptr, int64_t t_begin, int64_t t_end, int64_t row_begin,
+                  int64_t row_end, cudaStream_t s) {
+  if (C.nonempty && row_end > row_begin) {
+    k_csr5_empty_rows<<<grid_for(row_end - row_begin, 256, 148 * 32), 256, 0, s>>>(row_end - row_begin,
+                                                                                    ptr + row_begin, C.y + row_begin);
+    SPMVB_LAUNCHED("k_csr5_empty_rows");
+  }
+  launch_tiles(C, t_begin, t_end, s);
+}
+
 // First tile at or after `target` whose head starts a row (not a continuation).
 __global__ void k_csr5_range_starts(int64_t num_tiles, const uint32_t* __restrict__ aux, int n_ranges,
                                     int64_t* __restrict__ bounds) {
@@ -437,10 +450,6 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
     int dev = 0;
     SPMVB_CUDA(cudaGetDevice(&dev));
     cudaStream_t cs = copy_stream(dev);
-    if (nonempty_rows) {
-      k_csr5_empty_rows<<<grid_for(n_rows, 256, 148 * 32), 256, 0, s>>>(n_rows, ptr, y_dev);
-      SPMVB_LAUNCHED("k_csr5_empty_rows");
-    }
     Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
               nonempty_rows, carry, x_dev, y_dev, scale};
     std::vector<cudaEvent_t> evs;
@@ -458,8 +467,9 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
     for (int k = n_ranges - 1; k >= 0; --k) {
       const int64_t tb = tile_bounds[k], te = tile_bounds[k + 1];
       if (te < tb || te > num_tiles) fail(SPMVB_INVALID_ARG, "range plan is not monotone");
-      launch_tiles(C, tb, te, s);
       const int64_t lo = row_bounds[k], hi = k + 1 == n_ranges ? n_rows : row_bounds[k + 1];
+      if (lo < 0 || hi < lo || hi > n_rows) fail(SPMVB_INVALID_ARG, "range plan rows out of bounds");
+      launch_range(C, ptr, tb, te, lo, hi, s);
       if (hi > lo) {
         SPMVB_CUDA(cudaStreamWaitEvent(cs, event_on(s), 0));
         SPMVB_CUDA(cudaMemcpyAsync(y_host + lo, y_dev + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, cs));
@@ -468,5 +478,30 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
     SPMVB_CUDA(cudaStreamWaitEvent(s, event_on(cs), 0));
     SPMVB_CUDA(cudaStreamSynchronize(s));
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  });
+}
+
+extern "C" int spmvb_spmv_csr5_tiles(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                                     const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col,
+                                     const double* val, const uint32_t* tile_aux, const int32_t* nonempty_rows,
+                                     int64_t n_nonempty, double* carry, const double* x, double* y,
+                                     const double* scale, int64_t t_begin, int64_t t_end, int64_t row_begin,
+                                     int64_t row_end, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
+    const int64_t tile = static_cast<int64_t>(omega) * sigma;
+    const int64_t num_tiles = (nnz + tile - 1) / tile;
+    if (t_begin < 0 || t_end < t_begin || t_end > num_tiles || row_begin < 0 || row_end < row_begin ||
+        row_end > n_rows)
+      fail(SPMVB_INVALID_ARG, "tile/row range out of bounds");
+    if (nnz == 0) {
+      if (row_end > row_begin)
+        SPMVB_CUDA(cudaMemsetAsync(y + row_begin, 0, (row_end - row_begin) * sizeof(double), s));
+      return;
+    }
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
+              nonempty_rows, carry, x, y, scale};
+    launch_range(C, ptr, t_begin, t_end, row_begin, row_end, s);
   });
 }

@@ -25,7 +25,8 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import Csr5Matrix, CsrMatrix, EllMatrix, FormatMatrix, FormatTag, HybMatrix, SellMatrix
 
-__all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_ell", "spmv_hyb", "spmv_sell"]
+__all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_tiles", "spmv_ell", "spmv_hyb",
+           "spmv_sell"]
 
 
 def plan_row_blocks(n_rows: int, workers: int) -> list[tuple[int, int]]:
@@ -148,6 +149,32 @@ def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None, range
         )
 
     return _run(m, x, out, scale, launch)
+
+
+def spmv_csr5_tiles(m: Csr5Matrix, x: torch.Tensor, out: torch.Tensor, t_begin: int, t_end: int, row_begin: int,
+                    row_end: int, *, scale=None, carry: torch.Tensor | None = None) -> torch.Tensor:
+    """One range of a CSR5 SpMV on device buffers (spmvb_spmv_csr5_tiles):
+    zero the empty rows of [row_begin, row_end) and run tiles [t_begin,
+    t_end) with their fix-up.  Over the ranges of ``m.range_plan(k)``, in
+    any order, this equals ``spmv_csr5(m, x, out=out)`` bit for bit; the
+    multi-GPU power iteration sends each range's rows while the next one
+    computes.  ``carry``: num_tiles doubles of scratch (allocated if None)."""
+    xd = x.reshape(-1)
+    if not xd.is_cuda or xd.dtype != torch.float64 or xd.numel() != m.n_cols:
+        raise ValueError(f"x must be a float64 CUDA tensor of length {m.n_cols}")
+    y = _out(m, out)
+    if carry is None:
+        carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
+    with torch.cuda.device(m.device):
+        check(
+            LIB.spmvb_spmv_csr5_tiles(
+                m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag), ptr(m.indices),
+                ptr(m.data), ptr(m.tile_aux), ptr(m.nonempty_rows), m.n_nonempty, ptr(carry), ptr(xd.contiguous()),
+                ptr(y), ptr(scale) if scale is not None else None, int(t_begin), int(t_end), int(row_begin),
+                int(row_end), _lib.stream(m.device),
+            )
+        )
+    return y
 
 
 def _spmv_csr5_host(m: Csr5Matrix, x, out, scale, ranges: int):

@@ -24,13 +24,47 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _matrix(seed=3, n=300, density=0.03):
+def _matrix(seed=3, n=300, density=0.03, kind="random"):
     rng = np.random.default_rng(seed)
+    if kind == "banded":
+        # band |i-j| <= 6 plus a few long-range entries: shards read few columns
+        i = np.repeat(np.arange(n), 13)
+        j = i + np.tile(np.arange(-6, 7), n)
+        keep = (j >= 0) & (j < n)
+        extra = rng.integers(0, n, size=(40, 2))
+        r = np.concatenate([i[keep], extra[:, 0]])
+        c = np.concatenate([j[keep], extra[:, 1]])
+        r, c, v = port.canonicalize(r, c, rng.uniform(0.1, 1.0, r.size), n, n)
+        return port.to_csr(r, c, v, n), n
     nnz = int(density * n * n)
     flat = rng.choice(n * n, size=nnz, replace=False)
     r, c, v = port.canonicalize(flat // n, flat % n, rng.uniform(0.1, 1.0, nnz), n, n)
     # a few heavy rows make the nnz-balanced shards very different in rows
     return port.to_csr(r, c, v, n), n
+
+
+class CpuOps:
+    """CPU stand-ins for dist.GpuOps (same contracts)."""
+
+    @staticmethod
+    def sumsq(y, out_t):
+        out_t.fill_(float(torch.dot(y, y)))
+
+    @staticmethod
+    def inv_sqrt(s, scale):
+        scale.fill_(1.0 / float(torch.sqrt(s)))
+
+    @staticmethod
+    def column_set(cols, n_cols):
+        return torch.unique(cols.long()).to(torch.int32)
+
+    @staticmethod
+    def gather(src, base, idx, dst):
+        dst[: idx.numel()] = src[idx.long() - base]
+
+    @staticmethod
+    def scatter(src, idx, dst):
+        dst[idx.long()] = src[: idx.numel()]
 
 
 def _serial(ptr, ind, dat, n, x0, steps):
@@ -43,13 +77,13 @@ def _serial(ptr, ind, dat, n, x0, steps):
     return x, scale
 
 
-def _worker(rank, world, port_no, steps, out):
+def _worker(rank, world, port_no, steps, out, exchange="allgatherv", kind="random", ranges=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_no)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1805_11938_b200 import dist as spdist
 
-    (ptr, ind, dat), n = _matrix()
+    (ptr, ind, dat), n = _matrix(kind=kind)
     bounds = spdist.nnz_balanced_bounds(ptr, world)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     sub_ptr = ptr[lo:hi + 1] - ptr[lo]
@@ -59,18 +93,28 @@ def _worker(rank, world, port_no, steps, out):
         y = port.spmv_csr(sub_ptr, sub_ind, sub_dat, hi - lo, x.numpy())
         out_view.copy_(torch.from_numpy(y) * scale)
 
-    def sumsq(y, out_t):
-        out_t.fill_(float(torch.dot(y, y)))
+    spans, range_fn = None, None
+    if ranges:
+        # uneven spans (rank-dependent count), executed last to first
+        cuts = np.unique(np.linspace(0, hi - lo, ranges + rank + 1).astype(int))
+        spans = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])][::-1]
 
-    def inv_sqrt(s, scale):
-        scale.fill_(1.0 / float(torch.sqrt(s)))
+        def range_fn(k, x, out_view, scale):
+            a, b = spans[k]
+            p = sub_ptr[a:b + 1] - sub_ptr[a]
+            y = port.spmv_csr(p, sub_ind[sub_ptr[a]:sub_ptr[b]], sub_dat[sub_ptr[a]:sub_ptr[b]], b - a, x.numpy())
+            out_view[a:b].copy_(torch.from_numpy(y) * scale)
 
     x0 = torch.from_numpy(np.linspace(-1.0, 1.0, n))
-    pi = spdist.PowerIteration(local_spmv, bounds, rank, world, torch.device("cpu"), x0, sumsq=sumsq,
-                               inv_sqrt=inv_sqrt)
+    pi = spdist.PowerIteration(local_spmv, bounds, rank, world, torch.device("cpu"), x0, ops=CpuOps,
+                               exchange=exchange, local_cols=torch.from_numpy(sub_ind.astype(np.int32)),
+                               local_ranges=spans, local_spmv_range=range_fn)
     for _ in range(steps):
         pi.step()
-    out[rank] = (pi.x.numpy().copy(), float(pi.scale.item()), [int(b) for b in bounds])
+    partial = pi.x.numpy().copy()
+    vol = getattr(pi, "exchange_volume", None)
+    full = pi.gather_full().numpy().copy()
+    out[rank] = (full, float(pi.scale.item()), [int(b) for b in bounds], partial, np.unique(sub_ind), (lo, hi), vol)
     dist.destroy_process_group()
 
 
@@ -97,8 +141,48 @@ def test_two_rank_power_iteration_matches_serial():
     (ptr, ind, dat), n = _matrix()
     want_x, want_scale = _serial(ptr, ind, dat, n, np.linspace(-1.0, 1.0, n), steps)
     for rank in range(world):
-        x, scale, bounds = out[rank]
+        x, scale, bounds = out[rank][:3]
         # every rank holds the full gathered iterate
         np.testing.assert_allclose(x, want_x, rtol=1e-12, atol=1e-300)
         assert scale == pytest.approx(want_scale, rel=1e-12)
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("world,kind", [(2, "banded"), (3, "banded"), (2, "random")])
+def test_sparse_exchange_matches_serial(world, kind):
+    """exchange='sparse': each rank receives only the x entries its shard's
+    columns read; those entries (and its own rows) match the serial
+    iteration every step, and gather_full() restores the whole iterate."""
+    steps = 9
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), steps, out, "sparse", kind), nprocs=world, join=True)
+    (ptr, ind, dat), n = _matrix(kind=kind)
+    want_x, want_scale = _serial(ptr, ind, dat, n, np.linspace(-1.0, 1.0, n), steps)
+    for rank in range(world):
+        full, scale, bounds, partial, cols, (lo, hi), vol = out[rank]
+        np.testing.assert_allclose(full, want_x, rtol=1e-12, atol=1e-300)
+        assert scale == pytest.approx(want_scale, rel=1e-12)
+        read = np.union1d(cols, np.arange(lo, hi))
+        np.testing.assert_allclose(partial[read], want_x[read], rtol=1e-12, atol=1e-300)
+        remote = cols[(cols < lo) | (cols >= hi)]
+        assert vol["recv_entries"] == remote.size
+        if kind == "banded":
+            assert vol["recv_entries"] < vol["allgatherv_recv_entries"] / 4
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_overlapped_ranges_match_serial(world):
+    """All-gatherv overlapped with the local SpMV: each rank computes its rows
+    in (uneven, rank-dependent) spans and sends every span as soon as it is
+    done; the iterate matches the serial power iteration."""
+    steps = 8
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), steps, out, "allgatherv", "random", 3), nprocs=world, join=True)
+    (ptr, ind, dat), n = _matrix()
+    want_x, want_scale = _serial(ptr, ind, dat, n, np.linspace(-1.0, 1.0, n), steps)
+    for rank in range(world):
+        full, scale = out[rank][:2]
+        np.testing.assert_allclose(full, want_x, rtol=1e-12, atol=1e-300)
+        assert scale == pytest.approx(want_scale, rel=1e-12)

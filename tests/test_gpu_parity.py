@@ -174,6 +174,12 @@ def test_host_buffers(sp, rng):
                 inner = tb[1:-1][tb[1:-1] < m.num_tiles]
                 assert not np.any(aux[inner] >> 31), k  # ranges start at row-start tiles
                 assert same_bits(sp.spmv_csr5(m, x, ranges=k), yd), (kw, k)
+                # device ranges in shuffled order (the multi-GPU overlap path)
+                yt = torch.full((m.n_rows,), float("nan"), dtype=torch.float64, device="cuda")
+                for j in rng.permutation(len(tb) - 1):
+                    hi = int(rb[j + 1]) if j + 1 < len(tb) - 1 else m.n_rows
+                    sp.spmv_csr5_tiles(m, xd, yt, int(tb[j]), int(tb[j + 1]), int(rb[j]), hi)
+                assert same_bits(yt, yd), (kw, k)
     with pytest.raises(ValueError, match="out"):
         sp.spmv("csr", sp.to_csr(a), x, out=np.empty(3))
     # empty matrix / zero nnz through the host entry point
