@@ -16,19 +16,99 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Calls f(r) for every empty row r (ptr[r] == ptr[r+1]) in grid-stride
-// order; each ptr entry is loaded once (ptr[r+1] comes from the next lane).
+// Calls f(r) for every empty row r (ptr[r] == ptr[r+1]) of [0, n_rows);
+// block `bid` of `nb` blocks, warp-strided.  Each ptr entry is loaded once
+// (ptr[r+1] comes from the next lane) and four strides are loaded before any
+// is used, so a warp keeps four loads in flight.
+template <typename F>
+__device__ __forceinline__ void for_each_empty_row(int64_t n_rows, const int32_t* __restrict__ ptr, F f, int64_t bid,
+                                                   int64_t nb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = nb * blockDim.x;
+  constexpr int U = 4;
+  for (int64_t base = bid * blockDim.x + (threadIdx.x & ~31); base < n_rows; base += U * stride) {
+    int32_t p0[U], p1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // warp-uniform bounds (shuffles below)
+      const int64_t r = base + u * stride + lane;
+      p0[u] = r <= n_rows ? ld_stream(ptr + r) : 0;
+      p1[u] = (lane == 31 && r + 1 <= n_rows) ? ld_stream(ptr + r + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + u * stride + lane;
+      const int32_t nx = __shfl_down_sync(0xffffffffu, p0[u], 1);
+      if (lane != 31) p1[u] = nx;
+      if (r < n_rows && p0[u] == p1[u]) f(r);
+    }
+  }
+}
 template <typename F>
 __device__ __forceinline__ void for_each_empty_row(int64_t n_rows, const int32_t* __restrict__ ptr, F f) {
+  for_each_empty_row(n_rows, ptr, f, blockIdx.x, gridDim.x);
+}
+
+// Blocks to give an empty-row pass folded into a SpMV kernel's grid (it runs
+// alongside the gather-bound main blocks instead of as its own launch).
+inline int64_t empty_row_blocks(int64_t n_rows, int threads) {
+  const int64_t want = (n_rows + threads * 16 - 1) / (threads * 16);
+  return want < 148 * 2 ? want : 148 * 2;
+}
+
+// Folds chains of equal non-negative keys over items [begin, end): a chain is
+// a maximal run of consecutive items with the same key; apply(key, sum) gets
+// the chain's sum.  The sum is defined independently of how items map to
+// warps (so any split of the items into ranges gives the same bits): lane i
+// of a virtual warp sums items start+i, start+i+32, ... sequentially from
+// 0.0, and the 32 lane sums are combined by the xor butterfly of warp_sum.
+// One warp per 32-item window; the window holding a chain's first item owns
+// it.  Chains ending inside their window are evaluated by the start lane
+// alone (the same butterfly replayed in registers; one round of independent
+// loads); chains running past it are summed by the whole warp.
+template <typename Key, typename Val, typename Apply>
+__device__ __forceinline__ void fold_chains(int64_t begin, int64_t end, Key key_of, Val val_of, Apply apply) {
   const int lane = threadIdx.x & 31;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31); base < n_rows;
-       base += stride) {  // warp-uniform trip count (shuffles below)
-    const int64_t r = base + lane;
-    const int32_t p0 = r <= n_rows ? ld_stream(ptr + r) : 0;
-    int32_t p1 = __shfl_down_sync(0xffffffffu, p0, 1);
-    if (lane == 31) p1 = r + 1 <= n_rows ? ld_stream(ptr + r + 1) : 0;
-    if (r < n_rows && p0 == p1) f(r);
+  const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  auto key = [&](int64_t t) -> int32_t { return (t >= begin && t < end) ? key_of(t) : -1; };
+  for (int64_t w0 = begin + warp_id * 32; w0 < end; w0 += nwarps * 32) {
+    const int64_t t = w0 + lane;
+    const int32_t r = key(t);
+    int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
+    if (lane == 0) rp = key(t - 1);
+    const bool start = r >= 0 && rp != r;
+    const unsigned cont = __ballot_sync(0xffffffffu, r >= 0 && rp == r);
+    // lanes after this one that do NOT continue its chain
+    const unsigned breaks = lane == 31 ? 0u : (~cont) >> (lane + 1);
+    const int len = breaks ? __ffs(breaks) : 32 - lane;  // chain items inside the window
+    const bool spills = start && !breaks && key(w0 + 32) == r;
+    if (start && !spills) {
+      double u[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) u[i] = i < len ? 0.0 + val_of(t + i) : 0.0;
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) {
+#pragma unroll
+        for (int i = 0; i < d; ++i) u[i] = u[i] + u[i + d];
+      }
+      apply(r, u[0]);
+    }
+    unsigned longs = __ballot_sync(0xffffffffu, spills);
+    while (longs) {
+      const int l = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const int32_t k = __shfl_sync(0xffffffffu, r, l);
+      double acc = 0.0;
+      for (int64_t b = w0 + l;; b += 32) {
+        const int64_t tt = b + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, key(tt) == k);
+        const int n = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+        if (lane < n) acc += val_of(tt);
+        if (n < 32) break;
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) apply(k, acc);
+    }
   }
 }
 

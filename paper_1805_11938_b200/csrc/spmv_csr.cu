@@ -87,13 +87,23 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     const double* __restrict__ val, const int32_t* __restrict__ nz_rows, const int32_t* __restrict__ chunk_row,
     int64_t nchunks, int32_t* __restrict__ carry_row, double* __restrict__ carry_val, const double* __restrict__ x,
     double* __restrict__ y, const double* __restrict__ scale_p, int64_t ell_k, const int32_t* __restrict__ ell_idx,
-    const double* __restrict__ ell_val) {
+    const double* __restrict__ ell_val, int64_t empty_blocks) {
   static_assert(S == 8, "lane-contiguous loads assume 8 entries (32 B of indices) per lane");
   constexpr int CH = 32 * S;
+  if (blockIdx.x < empty_blocks) {
+    // empty rows (HYB: rows whose tail is empty get their ELL part), beside
+    // the gather-bound chunk blocks instead of as a separate launch
+    const double sc = load_scale(scale_p);
+    for_each_empty_row(
+        n_rows, ptr,
+        [&](int64_t r) { y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0; },
+        blockIdx.x, empty_blocks);
+    return;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem<S>& sm = *reinterpret_cast<ChunkSmem<S>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * CK_WARPS + w;
+  const int64_t c = static_cast<int64_t>(blockIdx.x - empty_blocks) * CK_WARPS + w;
   if (c >= nchunks) return;  // whole warps only
   const int64_t k0 = c * CH;
   const int cnt = static_cast<int>(nnz - k0 < CH ? nnz - k0 : CH);
@@ -195,43 +205,13 @@ __global__ void k_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, in
 }
 
 // Folds every chain of chunk carry-outs (consecutive chunks whose carry row is
-// the same) into its row: one warp per 32 chunks finds the chain starts, each
-// chain is summed by the whole warp 32 chunks per step with a fixed tree.
+// the same) into its row, chain by chain in chunk order (fold_chains).
 __global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row, const double* __restrict__ carry_val,
                               double* __restrict__ y, const double* __restrict__ scale_p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  auto key_of = [&](int64_t t) -> int32_t { return (t >= 0 && t < num) ? carry_row[t] : -1; };
   const double sc = load_scale(scale_p);
-  for (int64_t w0 = warp_id * 32; w0 < num; w0 += nwarps * 32) {
-    const int64_t cc = w0 + lane;
-    const int32_t r = key_of(cc);
-    int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
-    int32_t rn = __shfl_down_sync(0xffffffffu, r, 1);
-    if (lane == 0) rp = key_of(cc - 1);
-    if (lane == 31) rn = key_of(cc + 1);
-    const bool start = r >= 0 && rp != r;
-    const bool single = start && rn != r;  // a one-chunk chain: folded by its own lane
-    if (single) y[r] += sc * carry_val[cc];
-    unsigned starts = __ballot_sync(0xffffffffu, start && !single);
-    while (starts) {
-      const int l = __ffs(starts) - 1;
-      starts &= starts - 1;
-      const int32_t key = __shfl_sync(0xffffffffu, r, l);
-      double acc = 0.0;
-      for (int64_t b = w0 + l;; b += 32) {
-        const int64_t t = b + lane;
-        const bool in = key_of(t) == key;
-        const unsigned m = __ballot_sync(0xffffffffu, in);
-        const int len = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
-        if (lane < len) acc += carry_val[t];
-        if (len < 32) break;
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) y[key] += sc * acc;
-    }
-  }
+  fold_chains(
+      0, num, [&](int64_t c) { return carry_row[c]; }, [&](int64_t c) { return carry_val[c]; },
+      [&](int32_t r, double acc) { y[r] += sc * acc; });
 }
 
 constexpr int CHUNK_S = 8;  // entries per lane: one 256-bit load of indices
@@ -254,11 +234,12 @@ struct ChunkArgs {
 };
 
 template <int S, bool HAS_ELL, bool VEC>
-void launch_main(const ChunkArgs& a, int64_t nchunks, cudaStream_t s) {
+void launch_main(const ChunkArgs& a, int64_t nchunks, int64_t empty_blocks, cudaStream_t s) {
   const size_t smem = sizeof(ChunkSmem<S>);
-  k_spmv_chunk<S, HAS_ELL, VEC><<<static_cast<unsigned>((nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem,
-                                  s>>>(a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks,
-                                       a.carry_row, a.carry_val, a.x, a.y, a.scale, a.ell_k, a.ell_idx, a.ell_val);
+  k_spmv_chunk<S, HAS_ELL, VEC>
+      <<<static_cast<unsigned>(empty_blocks + (nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem, s>>>(
+          a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x, a.y,
+          a.scale, a.ell_k, a.ell_idx, a.ell_val, empty_blocks);
   SPMVB_LAUNCHED("k_spmv_chunk");
 }
 
@@ -266,15 +247,19 @@ template <int S, bool HAS_ELL>
 void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
   constexpr int CH = 32 * S;
   const int64_t nchunks = (a.nnz + CH - 1) / CH;
-  if (a.n_nz < a.n_rows) {  // empty rows (and, for HYB, rows whose tail is empty)
-    k_empty_rows<HAS_ELL><<<grid_for(a.n_rows, 256, 148 * 32), 256, 0, s>>>(
-        a.n_rows, a.nnz > 0 ? a.ptr : nullptr, a.ell_k, a.ell_idx, a.ell_val, a.x, a.y, a.scale);
-    SPMVB_LAUNCHED("k_empty_rows");
+  const bool empties = a.n_nz < a.n_rows;  // empty rows (and, for HYB, rows whose tail is empty)
+  if (nchunks == 0) {
+    if (empties) {
+      k_empty_rows<HAS_ELL><<<grid_for(a.n_rows, 256, 148 * 32), 256, 0, s>>>(a.n_rows, nullptr, a.ell_k, a.ell_idx,
+                                                                              a.ell_val, a.x, a.y, a.scale);
+      SPMVB_LAUNCHED("k_empty_rows");
+    }
+    return;
   }
-  if (nchunks == 0) return;
+  const int64_t eb = empties ? empty_row_blocks(a.n_rows, CK_WARPS * 32) : 0;
   // 256-bit loads need 32-byte aligned index/value arrays (torch allocations are)
-  if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, s);
-  else launch_main<S, HAS_ELL, false>(a, nchunks, s);
+  if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, eb, s);
+  else launch_main<S, HAS_ELL, false>(a, nchunks, eb, s);
   if (nchunks > 1) {
     k_chunk_fixup<<<grid_for(nchunks, 256, 148 * 8), 256, 0, s>>>(nchunks, a.carry_row, a.carry_val, a.y, a.scale);
     SPMVB_LAUNCHED("k_chunk_fixup");

@@ -20,6 +20,7 @@ namespace {
 struct Csr5Ctx {
   int64_t n_rows, nnz, n_nonempty;
   int omega, sigma;
+  const int32_t* ptr;
   const int32_t* tile_ptr;
   const uint8_t* bit_flag;
   const int32_t* col;
@@ -141,12 +142,23 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
 // Same algorithm with a compile-time sigma: each lane issues its S flag,
 // column and value loads back to back, then S independent x gathers, so a
 // warp keeps 32*S gathers in flight (random-column matrices are bound by the
-// L1TEX wavefront rate of these gathers, ~2 cycles per distinct line).
-template <int W, int S, bool PARTIAL>
-__global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end) {
+// L1TEX rate of these gathers, ~1 distinct line per SM cycle).  The trailing
+// partial tile (row-major over its occupied cells, formats.py:24-25) takes a
+// different load path in the same kernel.  The first `empty_blocks` blocks
+// instead zero the empty rows of [row_begin, row_end): that streaming pass
+// runs beside the gather-bound tile blocks rather than as its own launch.
+template <int W, int S>
+__global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
+                                                     int64_t empty_blocks, int64_t row_begin, int64_t row_end) {
+  if (blockIdx.x < empty_blocks) {
+    double* yb = C.y + row_begin;
+    for_each_empty_row(row_end - row_begin, C.ptr + row_begin, [&](int64_t r) { yb[r] = 0.0; }, blockIdx.x,
+                       empty_blocks);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
-  const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
+  const int64_t group = t_begin + ((blockIdx.x - empty_blocks) * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
   const bool active = group < t_end;
   const int64_t t = active ? group : t_begin;
   const int64_t tile0 = t * static_cast<int64_t>(W) * S;
@@ -154,28 +166,37 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
   uint32_t fmask = 0;
   int32_t cidx[S];
   double v[S];
-  if (!PARTIAL) {
+  if (active && tile0 + W * S <= C.nnz) {
     const int64_t base = tile0 + j;
-    if (active) {
-#pragma unroll
-      for (int i = 0; i < S; ++i) {
-        fmask |= (C.bit_flag[base + i * W] ? 1u : 0u) << i;
-        cidx[i] = ld_stream(C.col + base + i * W);
-        v[i] = ld_stream(C.val + base + i * W);
-      }
-#pragma unroll
-      for (int i = 0; i < S; ++i) v[i] *= ldx(C.x, cidx[i]);
-    }
-  } else {
-    // trailing partial tile: row-major over occupied cells (formats.py:24-25)
-    const int64_t m = C.nnz - tile0;
-    const int q = static_cast<int>(m / S), rem = static_cast<int>(m % S);
 #pragma unroll
     for (int i = 0; i < S; ++i) {
-      const bool ok = active && static_cast<int64_t>(j) * S + i < m;
-      const int64_t pos = tile0 + static_cast<int64_t>(i) * q + (i < rem ? i : rem) + j;
-      fmask |= (ok && C.bit_flag[pos] ? 1u : 0u) << i;
-      v[i] = ok ? C.val[pos] * ldx(C.x, C.col[pos]) : 0.0;
+      fmask |= (C.bit_flag[base + i * W] ? 1u : 0u) << i;
+      cidx[i] = ld_stream(C.col + base + i * W);
+      v[i] = ld_stream(C.val + base + i * W);
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) v[i] *= ldx(C.x, cidx[i]);
+  } else if (active) {
+    // partial tile: every load is issued (clamped to the tile start when the
+    // cell is unoccupied) before any is used
+    const int64_t m = C.nnz - tile0;
+    const int q = static_cast<int>(m / S), rem = static_cast<int>(m % S);
+    uint32_t okm = 0;
+    uint8_t fl[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const bool ok = static_cast<int64_t>(j) * S + i < m;
+      okm |= (ok ? 1u : 0u) << i;
+      const int64_t pos = ok ? tile0 + static_cast<int64_t>(i) * q + (i < rem ? i : rem) + j : tile0;
+      fl[i] = C.bit_flag[pos];
+      cidx[i] = C.col[pos];
+      v[i] = C.val[pos];
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const bool ok = (okm >> i) & 1u;
+      fmask |= (ok && fl[i] ? 1u : 0u) << i;
+      v[i] = ok ? v[i] * ldx(C.x, cidx[i]) : 0.0;
     }
   }
   const uint32_t aux = active ? C.aux[t] : 0u;
@@ -219,101 +240,80 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
   if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
 }
 
+// Carry fix-up of the continuation chains (consecutive tiles whose head
+// continues the same row) inside [t_begin, t_end), chain by chain in tile
+// order (fold_chains); the carries are already scaled.
 __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __restrict__ tile_ptr,
                              const uint32_t* __restrict__ aux, const double* __restrict__ carry, double* __restrict__ y) {
-  // Chains of continuation tiles (consecutive tiles whose head continues the
-  // same row) inside [t_begin, t_end).  A chain of one tile — the common
-  // case — is folded by its own lane; longer chains are folded
-  // warp-cooperatively 32 tiles per step, relative to the chain start.
-  const int lane = threadIdx.x & 31;
-  const int64_t warp_id = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  auto key_of = [&](int64_t t) -> int32_t {  // continued row of tile t, or -1
-    return (t >= t_begin && t < t_end && (aux[t] & 0x80000000u)) ? tile_ptr[t] : -1;
-  };
-  for (int64_t w0 = t_begin + warp_id * 32; w0 < t_end; w0 += nwarps * 32) {
-    const int64_t t = w0 + lane;
-    const int32_t r = key_of(t);
-    int32_t rp = __shfl_up_sync(0xffffffffu, r, 1);
-    int32_t rn = __shfl_down_sync(0xffffffffu, r, 1);
-    if (lane == 0) rp = key_of(t - 1);
-    if (lane == 31) rn = key_of(t + 1);
-    const bool start = r >= 0 && rp != r;
-    const bool single = start && rn != r;
-    if (single) y[r] = y[r] + carry[t];
-    unsigned starts = __ballot_sync(0xffffffffu, start && !single);
-    while (starts) {
-      const int l = __ffs(starts) - 1;
-      starts &= starts - 1;
-      const int32_t key = __shfl_sync(0xffffffffu, r, l);
-      double acc = 0.0;
-      for (int64_t b = w0 + l;; b += 32) {
-        const int64_t tt = b + lane;
-        const bool in = key_of(tt) == key;
-        const unsigned m = __ballot_sync(0xffffffffu, in);
-        const int len = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
-        if (lane < len) acc += carry[tt];
-        if (len < 32) break;
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) y[key] = y[key] + acc;
-    }
-  }
+  fold_chains(
+      t_begin, t_end, [&](int64_t t) -> int32_t { return (aux[t] & 0x80000000u) ? tile_ptr[t] : -1; },
+      [&](int64_t t) { return carry[t]; }, [&](int32_t r, double acc) { y[r] = y[r] + acc; });
 }
 
-// Tiles [t_begin, t_end) of one SpMV: the per-tile kernel(s), then the carry
-// fix-up of the continuation chains inside the range.  A range that starts at
-// a non-continuation tile folds exactly like the whole matrix would.
-void launch_tiles(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, cudaStream_t s) {
-  if (t_end <= t_begin) return;
+// One range of tiles, [t_begin, t_end), with the empty rows of [row_begin,
+// row_end): the per-tile kernel(s), then the carry fix-up of the chains
+// inside the range.  Ranges that start at row-start tiles (the range plan)
+// fold exactly like the whole matrix, in any order.
+void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_begin, int64_t row_end,
+                  cudaStream_t s) {
+  const bool empties = C.nonempty && row_end > row_begin;
+  auto empty_pass = [&] {
+    if (empties) {
+      k_csr5_empty_rows<<<grid_for(row_end - row_begin, 256, 148 * 32), 256, 0, s>>>(
+          row_end - row_begin, C.ptr + row_begin, C.y + row_begin);
+      SPMVB_LAUNCHED("k_csr5_empty_rows");
+    }
+  };
+  if (t_end <= t_begin) {
+    empty_pass();
+    return;
+  }
   const int64_t tile = static_cast<int64_t>(C.omega) * C.sigma;
   const int64_t full = C.nnz / tile;
   const int64_t fe = t_end < full ? t_end : full;  // full tiles in range: [t_begin, fe)
   int64_t generic_begin = t_begin;
   auto warp_launch = [&](auto kern, int W) {
+    empty_pass();
     if (fe > t_begin) {
       kern<<<grid_for((fe - t_begin) * W, 256), 256, 0, s>>>(C, t_begin, fe);
       SPMVB_LAUNCHED("k_csr5_warp");
       generic_begin = fe;
     }
   };
-  auto warp_s_launch = [&](auto kern, auto kern_partial, int W) {  // full tiles, then the partial one
-    if (fe > t_begin) {
-      kern<<<grid_for((fe - t_begin) * W, 256), 256, 0, s>>>(C, t_begin, fe);
-      SPMVB_LAUNCHED("k_csr5_warp_s");
-    }
-    if (t_end > fe && t_end > full) {
-      kern_partial<<<1, 32, 0, s>>>(C, full, t_end);
-      SPMVB_LAUNCHED("k_csr5_warp_s_partial");
-    }
+  auto warp_s_launch = [&](auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
+    const int64_t eb = empties ? empty_row_blocks(row_end - row_begin, 256) : 0;
+    kern<<<static_cast<unsigned>(eb + (t_end - t_begin) * W / 256 + ((t_end - t_begin) * W % 256 ? 1 : 0)), 256, 0,
+           s>>>(C, t_begin, t_end, eb, row_begin, row_end);
+    SPMVB_LAUNCHED("k_csr5_warp_s");
     generic_begin = t_end;
   };
   const int omega = C.omega, sigma = C.sigma;
   if ((sigma == 16 || sigma == 8) && (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
     if (sigma == 16) {
       switch (omega) {
-        case 32: warp_s_launch(k_csr5_warp_s<32, 16, false>, k_csr5_warp_s<32, 16, true>, 32); break;
-        case 16: warp_s_launch(k_csr5_warp_s<16, 16, false>, k_csr5_warp_s<16, 16, true>, 16); break;
-        case 8: warp_s_launch(k_csr5_warp_s<8, 16, false>, k_csr5_warp_s<8, 16, true>, 8); break;
-        default: warp_s_launch(k_csr5_warp_s<4, 16, false>, k_csr5_warp_s<4, 16, true>, 4); break;
+        case 32: warp_s_launch(k_csr5_warp_s<32, 16>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 16>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 16>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 16>, 4); break;
       }
     } else {
       switch (omega) {
-        case 32: warp_s_launch(k_csr5_warp_s<32, 8, false>, k_csr5_warp_s<32, 8, true>, 32); break;
-        case 16: warp_s_launch(k_csr5_warp_s<16, 8, false>, k_csr5_warp_s<16, 8, true>, 16); break;
-        case 8: warp_s_launch(k_csr5_warp_s<8, 8, false>, k_csr5_warp_s<8, 8, true>, 8); break;
-        default: warp_s_launch(k_csr5_warp_s<4, 8, false>, k_csr5_warp_s<4, 8, true>, 4); break;
+        case 32: warp_s_launch(k_csr5_warp_s<32, 8>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 8>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 8>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 8>, 4); break;
       }
     }
-  } else if (sigma <= 1024) {
+  } else if (sigma <= 1024 && (omega == 32 || omega == 16 || omega == 8 || omega == 4 || omega == 2)) {
     switch (omega) {
       case 32: warp_launch(k_csr5_warp<32>, 32); break;
       case 16: warp_launch(k_csr5_warp<16>, 16); break;
       case 8: warp_launch(k_csr5_warp<8>, 8); break;
       case 4: warp_launch(k_csr5_warp<4>, 4); break;
-      case 2: warp_launch(k_csr5_warp<2>, 2); break;
-      default: break;
+      default: warp_launch(k_csr5_warp<2>, 2); break;
     }
+  } else {
+    empty_pass();
   }
   if (generic_begin < t_end) {
     k_csr5_generic<<<grid_for(t_end - generic_begin, 128, 148 * 64), 128, 0, s>>>(C, generic_begin, t_end);
@@ -324,19 +324,6 @@ void launch_tiles(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, cudaStream_t
                                                                          C.y);
     SPMVB_LAUNCHED("k_csr5_fixup");
   }
-}
-
-// One range of a range plan: zero the empty rows of [row_begin, row_end),
-// then tiles [t_begin, t_end) with their fix-up.  Row-aligned ranges (each
-// starting at a row-start tile) may run in any order.
-void launch_range(const Csr5Ctx& C, const int32_t* ptr, int64_t t_begin, int64_t t_end, int64_t row_begin,
-                  int64_t row_end, cudaStream_t s) {
-  if (C.nonempty && row_end > row_begin) {
-    k_csr5_empty_rows<<<grid_for(row_end - row_begin, 256, 148 * 32), 256, 0, s>>>(row_end - row_begin,
-                                                                                    ptr + row_begin, C.y + row_begin);
-    SPMVB_LAUNCHED("k_csr5_empty_rows");
-  }
-  launch_tiles(C, t_begin, t_end, s);
 }
 
 // First tile at or after `target` whose head starts a row (not a continuation).
@@ -380,14 +367,10 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, 
       return;
     }
     if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
-    if (nonempty_rows) {
-      k_csr5_empty_rows<<<grid_for(n_rows, 256, 148 * 32), 256, 0, s>>>(n_rows, ptr, y);
-      SPMVB_LAUNCHED("k_csr5_empty_rows");
-    }
-    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, col, val, tile_aux,
               nonempty_rows, carry, x, y, scale};
     const int64_t tile = static_cast<int64_t>(omega) * sigma;
-    launch_tiles(C, 0, (nnz + tile - 1) / tile, s);
+    launch_range(C, 0, (nnz + tile - 1) / tile, 0, n_rows, s);
   });
 }
 
@@ -450,7 +433,7 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
     int dev = 0;
     SPMVB_CUDA(cudaGetDevice(&dev));
     cudaStream_t cs = copy_stream(dev);
-    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, col, val, tile_aux,
               nonempty_rows, carry, x_dev, y_dev, scale};
     std::vector<cudaEvent_t> evs;
     auto event_on = [&](cudaStream_t st) {
@@ -469,7 +452,7 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
       if (te < tb || te > num_tiles) fail(SPMVB_INVALID_ARG, "range plan is not monotone");
       const int64_t lo = row_bounds[k], hi = k + 1 == n_ranges ? n_rows : row_bounds[k + 1];
       if (lo < 0 || hi < lo || hi > n_rows) fail(SPMVB_INVALID_ARG, "range plan rows out of bounds");
-      launch_range(C, ptr, tb, te, lo, hi, s);
+      launch_range(C, tb, te, lo, hi, s);
       if (hi > lo) {
         SPMVB_CUDA(cudaStreamWaitEvent(cs, event_on(s), 0));
         SPMVB_CUDA(cudaMemcpyAsync(y_host + lo, y_dev + lo, (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost, cs));
@@ -500,8 +483,8 @@ extern "C" int spmvb_spmv_csr5_tiles(int64_t n_rows, int64_t nnz, const int32_t*
         SPMVB_CUDA(cudaMemsetAsync(y + row_begin, 0, (row_end - row_begin) * sizeof(double), s));
       return;
     }
-    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, tile_ptr, bit_flag, col, val, tile_aux,
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, col, val, tile_aux,
               nonempty_rows, carry, x, y, scale};
-    launch_range(C, ptr, t_begin, t_end, row_begin, row_end, s);
+    launch_range(C, t_begin, t_end, row_begin, row_end, s);
   });
 }
