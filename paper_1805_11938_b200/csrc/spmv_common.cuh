@@ -112,6 +112,80 @@ __device__ __forceinline__ void fold_chains(int64_t begin, int64_t end, Key key_
   }
 }
 
+// Sequential row sum over k slots at base + j*stride (ELL/SELL column-major
+// grids): acc = ((0 + v0*x[c0]) + v1*x[c1]) + ..., separately rounded
+// products, exactly the reference recurrence (kernels.py:101-104).  Four
+// slots per step; the next four slots' loads are issued before this step's
+// x gathers are consumed (unpredicated full steps, then a scalar tail).
+__device__ __forceinline__ double seq_slots(int64_t k, int64_t stride, int64_t base, const int32_t* __restrict__ idx,
+                                            const double* __restrict__ val, const double* __restrict__ x) {
+  double acc = 0.0;
+  int64_t j = 0;
+  if (k >= 4) {
+    int32_t c[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = ld_stream(idx + base + u * stride);
+      v[u] = ld_stream(val + base + u * stride);
+    }
+    for (; j + 8 <= k; j += 4) {
+      int32_t cn[4];
+      double vn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cn[u] = ld_stream(idx + base + (j + 4 + u) * stride);
+        vn[u] = ld_stream(val + base + (j + 4 + u) * stride);
+      }
+      double xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = ldx(x, c[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+    }
+    double xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = ldx(x, c[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    j += 4;
+  }
+  for (; j < k; ++j) {
+    const int64_t o = base + j * stride;
+    acc = __dadd_rn(acc, __dmul_rn(ld_stream(val + o), ldx(x, ld_stream(idx + o))));
+  }
+  return acc;
+}
+
+// The same recurrence four slots at a time without the prefetch: fewer
+// registers, so more resident threads -- better for short rows (k <= 8).
+__device__ __forceinline__ double seq_slots4(int64_t k, int64_t stride, int64_t base, const int32_t* __restrict__ idx,
+                                             const double* __restrict__ val, const double* __restrict__ x) {
+  double acc = 0.0;
+  int64_t j = 0;
+  for (; j + 4 <= k; j += 4) {
+    const int64_t o = base + j * stride;
+    const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + stride);
+    const double v2 = ld_stream(val + o + 2 * stride), v3 = ld_stream(val + o + 3 * stride);
+    const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + stride);
+    const int32_t c2 = ld_stream(idx + o + 2 * stride), c3 = ld_stream(idx + o + 3 * stride);
+    acc = __dadd_rn(acc, __dmul_rn(v0, ldx(x, c0)));
+    acc = __dadd_rn(acc, __dmul_rn(v1, ldx(x, c1)));
+    acc = __dadd_rn(acc, __dmul_rn(v2, ldx(x, c2)));
+    acc = __dadd_rn(acc, __dmul_rn(v3, ldx(x, c3)));
+  }
+  for (; j < k; ++j) {
+    const int64_t o = base + j * stride;
+    acc = __dadd_rn(acc, __dmul_rn(ld_stream(val + o), ldx(x, ld_stream(idx + o))));
+  }
+  return acc;
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 

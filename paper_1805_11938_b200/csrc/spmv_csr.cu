@@ -58,27 +58,8 @@ template <bool HAS_ELL>
 __device__ __forceinline__ double ell_row(int64_t n_rows, int64_t r, int64_t ell_k, const int32_t* __restrict__ ell_idx,
                                           const double* __restrict__ ell_val, const double* __restrict__ x) {
   // sequential over the K slots with separately rounded products, as the
-  // reference's spmv_ell (kernels.py:101-104); loads issued 4 slots ahead
-  double e = 0.0;
-  if (HAS_ELL) {
-    int64_t j = 0;
-    for (; j + 4 <= ell_k; j += 4) {
-      const int64_t o = j * n_rows + r;
-      const double v0 = ld_stream(ell_val + o), v1 = ld_stream(ell_val + o + n_rows);
-      const double v2 = ld_stream(ell_val + o + 2 * n_rows), v3 = ld_stream(ell_val + o + 3 * n_rows);
-      const int32_t c0 = ld_stream(ell_idx + o), c1 = ld_stream(ell_idx + o + n_rows);
-      const int32_t c2 = ld_stream(ell_idx + o + 2 * n_rows), c3 = ld_stream(ell_idx + o + 3 * n_rows);
-      e = __dadd_rn(e, __dmul_rn(v0, ldx(x, c0)));
-      e = __dadd_rn(e, __dmul_rn(v1, ldx(x, c1)));
-      e = __dadd_rn(e, __dmul_rn(v2, ldx(x, c2)));
-      e = __dadd_rn(e, __dmul_rn(v3, ldx(x, c3)));
-    }
-    for (; j < ell_k; ++j) {
-      const int64_t o = j * n_rows + r;
-      e = __dadd_rn(e, __dmul_rn(ld_stream(ell_val + o), ldx(x, ld_stream(ell_idx + o))));
-    }
-  }
-  return e;
+  // reference's spmv_ell (kernels.py:101-104)
+  return HAS_ELL ? seq_slots4(ell_k, n_rows, r, ell_idx, ell_val, x) : 0.0;
 }
 
 template <int S, bool HAS_ELL, bool VEC>
@@ -309,6 +290,11 @@ extern "C" int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx,
                               int32_t* carry_row, double* carry_val, const double* x, double* y, const double* scale,
                               void* stream) {
   return guard([&] {
+    if (tail_nnz == 0 && k > 0) {  // empty tail: the ELL part is the whole result
+      const int rc = spmvb_spmv_ell(n_rows, k, ell_idx, ell_val, x, y, scale, stream);
+      if (rc != SPMVB_OK) fail(rc, "%s", spmvb_last_error());
+      return;
+    }
     launch_chunk(ChunkArgs{n_rows, tail_nnz, tail_ptr, tail_col, tail_val, nz_rows, chunk_row, n_nz, carry_row,
                            carry_val, x, y, scale, k, ell_idx, ell_val},
                  as_stream(stream));

@@ -8,28 +8,17 @@ using namespace spmvb;
 namespace {
 
 // ================================================================ ELL ====
+// Thread per row over the column-major grid (coalesced slot loads), the
+// reference's sequential slot recurrence (bit-identical).  PF: the next four
+// slots' loads are in flight while the current four are summed (k > 8);
+// without it more threads fit per SM (short rows).
+template <bool PF>
 __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict__ idx, const double* __restrict__ val,
                            const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
   const double s = load_scale(scale_p);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double acc = 0.0;
-    int64_t j = 0;
-    for (; j + 4 <= k; j += 4) {
-      const int64_t o = j * n_rows + r;
-      const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + n_rows);
-      const double v2 = ld_stream(val + o + 2 * n_rows), v3 = ld_stream(val + o + 3 * n_rows);
-      const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + n_rows);
-      const int32_t c2 = ld_stream(idx + o + 2 * n_rows), c3 = ld_stream(idx + o + 3 * n_rows);
-      acc = __dadd_rn(acc, __dmul_rn(v0, ldx(x, c0)));
-      acc = __dadd_rn(acc, __dmul_rn(v1, ldx(x, c1)));
-      acc = __dadd_rn(acc, __dmul_rn(v2, ldx(x, c2)));
-      acc = __dadd_rn(acc, __dmul_rn(v3, ldx(x, c3)));
-    }
-    for (; j < k; ++j) {
-      const int64_t o = j * n_rows + r;
-      acc = __dadd_rn(acc, __dmul_rn(ld_stream(val + o), ldx(x, ld_stream(idx + o))));
-    }
+    const double acc = PF ? seq_slots(k, n_rows, r, idx, val, x) : seq_slots4(k, n_rows, r, idx, val, x);
     y[r] = scale_p ? s * acc : acc;
   }
 }
@@ -46,24 +35,7 @@ __global__ void k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict
     const int64_t rows_s = (sl + 1) * c <= n_rows ? c : n_rows - sl * c;
     const int64_t w = widths[sl];
     if (w > SPMVB_SELL_WIDE_COLS && rows_s <= 128) continue;  // k_spmv_sell_wide's slice
-    const int64_t o0 = slice_off[sl] + local;
-    double acc = 0.0;
-    int64_t j = 0;
-    for (; j + 4 <= w; j += 4) {
-      const int64_t o = o0 + j * rows_s;
-      const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + rows_s);
-      const double v2 = ld_stream(val + o + 2 * rows_s), v3 = ld_stream(val + o + 3 * rows_s);
-      const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + rows_s);
-      const int32_t c2 = ld_stream(idx + o + 2 * rows_s), c3 = ld_stream(idx + o + 3 * rows_s);
-      acc = __dadd_rn(acc, __dmul_rn(v0, ldx(x, c0)));
-      acc = __dadd_rn(acc, __dmul_rn(v1, ldx(x, c1)));
-      acc = __dadd_rn(acc, __dmul_rn(v2, ldx(x, c2)));
-      acc = __dadd_rn(acc, __dmul_rn(v3, ldx(x, c3)));
-    }
-    for (; j < w; ++j) {
-      const int64_t o = o0 + j * rows_s;
-      acc = __dadd_rn(acc, __dmul_rn(ld_stream(val + o), ldx(x, ld_stream(idx + o))));
-    }
+    const double acc = seq_slots4(w, rows_s, slice_off[sl] + local, idx, val, x);
     const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
     y[r] = scale_p ? s * acc : acc;
   }
@@ -159,7 +131,8 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
-    k_spmv_ell<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, k, idx, val, x, y, scale);
+    if (k > 8) k_spmv_ell<true><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, k, idx, val, x, y, scale);
+    else k_spmv_ell<false><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, k, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_ell");
   });
 }
