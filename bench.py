@@ -267,6 +267,22 @@ def run_ours(args):
             traffic = json.loads(tf.read_text()).get(f"{args.workload}/{tag}/n{world}")
         except ValueError:
             traffic = None
+    # Gather ceiling, measured live: on power-law matrices the SpMV is bound by
+    # the L1TEX rate of its random x gathers, not by HBM.  spmvb_gather_probe
+    # sums x at this shard's own column indices (all of them, same x, no
+    # arithmetic, no stores) -- a rate the SpMV cannot exceed.
+    gpart = torch.empty(int(_lib.load().spmvb_gather_probe_threads()), dtype=torch.float64, device=dev)
+    stream_ptr = torch.cuda.current_stream(dev).cuda_stream
+
+    def probe():
+        _lib.check(_lib.load().spmvb_gather_probe(x_full.data_ptr(), shard.indices.data_ptr(), shard.nnz,
+                                                  gpart.data_ptr(), stream_ptr))
+
+    t_gather = event_time(probe, reps=10)
+    del gpart
+    gather = {"gathers_per_launch": int(m.nnz), "achieved_G_per_s": m.nnz / t_kernel / 1e9,
+              "peak_G_per_s": shard.nnz / t_gather / 1e9, "frac": (m.nnz / t_kernel) / (shard.nnz / t_gather),
+              "peak_source": "spmvb_gather_probe: x summed at all of this shard's column indices (CUDA events)"}
 
     # ---- timed power iteration ----
     def local_spmv(xv, out, scale):
@@ -398,7 +414,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": f"spmv_{tag} (rank 0 shard)", "bytes_per_launch": bytes_model,
-                         "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0},
+                         "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0,
+                         "gather_bound": gather},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

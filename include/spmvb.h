@@ -278,6 +278,13 @@ int spmvb_column_set(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* c
 int spmvb_gather_f64(const double* src, int64_t base, const int32_t* idx, int64_t n, double* dst, void* stream);
 int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream);
 
+/* Roofline probe (bench.py): partial[t] = sum of src[idx[i]] over thread t's
+ * share of [0, n), 16 gathers in flight per thread, no per-element stores --
+ * the L1TEX rate of a matrix's x gathers, which its SpMV cannot beat.
+ * partial holds spmvb_gather_probe_threads() doubles. */
+int64_t spmvb_gather_probe_threads(void);
+int spmvb_gather_probe(const double* src, const int32_t* idx, int64_t n, double* partial, void* stream);
+
 /* ======================================================================== */
 /* Features — replaces features.py:69-84 (extract_features)                 */
 /* ======================================================================== */

@@ -70,6 +70,24 @@ int guard(F&& f) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// The stream-ordered pool returns freed memory to the driver at every
+// synchronization by default (release threshold 0), so a conversion that
+// syncs between phases re-maps its multi-GB temporaries each call.  Keep up
+// to 16 GB cached per device (cheap against 180 GB of HBM).
+inline void pool_keep_memory() {
+  static std::atomic<uint64_t> done_mask{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  const uint64_t bit = 1ull << dev;
+  if (done_mask.load(std::memory_order_relaxed) & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = 16ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_mask.fetch_or(bit);
+}
+
 // Stream-ordered temporary device buffer (cudaMallocAsync / cudaFreeAsync).
 template <typename T>
 struct DevBuf {
@@ -78,7 +96,10 @@ struct DevBuf {
   cudaStream_t stream = nullptr;
   DevBuf() = default;
   DevBuf(size_t n, cudaStream_t s) : count(n), stream(s) {
-    if (n) SPMVB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), s));
+    if (n) {
+      pool_keep_memory();
+      SPMVB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), s));
+    }
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;

@@ -3,7 +3,7 @@
 // whole all-gathered vector.  Setup finds the shard's column set; every step
 // the owner gathers the requested entries of its y block into one send
 // buffer and the receiver scatters them into its x.
-#include "prims.cuh"
+#include "spmv_common.cuh"
 
 using namespace spmvb;
 
@@ -15,18 +15,64 @@ __global__ void k_mark_columns(const int32_t* __restrict__ col, int64_t nnz, uin
     flags[col[k]] = 1;
 }
 
+// Eight independent gathers in flight per thread (the L1TEX-bound regime:
+// one distinct line per SM cycle needs thousands of loads outstanding).
+constexpr int GU = 8;
+
 __global__ void k_gather_f64(const double* __restrict__ src, int64_t base, const int32_t* __restrict__ idx, int64_t n,
                              double* __restrict__ dst) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    dst[i] = src[idx[i] - base];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + (GU - 1) * stride < n; i += GU * stride) {
+    int32_t c[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) c[u] = ld_stream(idx + i + u * stride);
+    double v[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) v[u] = __ldg(src + (c[u] - base));
+#pragma unroll
+    for (int u = 0; u < GU; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < n; i += stride) dst[i] = __ldg(src + (idx[i] - base));
 }
 
 __global__ void k_scatter_f64(const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                               double* __restrict__ dst) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    dst[idx[i]] = src[i];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + (GU - 1) * stride < n; i += GU * stride) {
+    int32_t c[GU];
+    double v[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      c[u] = ld_stream(idx + i + u * stride);
+      v[u] = ld_stream(src + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < GU; ++u) dst[c[u]] = v[u];
+  }
+  for (; i < n; i += stride) dst[idx[i]] = src[i];
+}
+
+// Gather-rate probe: sum of src[idx[i]] per thread (no per-element stores),
+// sixteen gathers in flight per thread.  The SpMV of the same columns can
+// only be slower: it is the roofline's L1TEX gather ceiling.
+__global__ void k_gather_sum(const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                             double* __restrict__ partial) {
+  constexpr int U = 16;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  double acc = 0.0;
+  int64_t i = tid;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    int32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = ld_stream(idx + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += __ldg(src + c[u]);
+  }
+  for (; i < n; i += stride) acc += __ldg(src + idx[i]);
+  partial[tid] = acc;
 }
 
 }  // namespace
@@ -60,7 +106,7 @@ extern "C" int spmvb_gather_f64(const double* src, int64_t base, const int32_t* 
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n <= 0) return;
-    k_gather_f64<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(src, base, idx, n, dst);
+    k_gather_f64<<<grid_for(n, 256 * GU, 148 * 8), 256, 0, s>>>(src, base, idx, n, dst);
     SPMVB_LAUNCHED("k_gather_f64");
   });
 }
@@ -69,7 +115,17 @@ extern "C" int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t 
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n <= 0) return;
-    k_scatter_f64<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(src, idx, n, dst);
+    k_scatter_f64<<<grid_for(n, 256 * GU, 148 * 8), 256, 0, s>>>(src, idx, n, dst);
     SPMVB_LAUNCHED("k_scatter_f64");
+  });
+}
+
+extern "C" int64_t spmvb_gather_probe_threads(void) { return 148 * 8 * 256; }
+
+extern "C" int spmvb_gather_probe(const double* src, const int32_t* idx, int64_t n, double* partial, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    k_gather_sum<<<148 * 8, 256, 0, s>>>(src, idx, n, partial);
+    SPMVB_LAUNCHED("k_gather_sum");
   });
 }

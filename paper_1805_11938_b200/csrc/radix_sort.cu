@@ -16,10 +16,20 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
   __syncthreads();
   int64_t base = static_cast<int64_t>(blockIdx.x) * RS_TILE;
   const unsigned lane = threadIdx.x & 31;
-  for (int i = 0; i < RS_TILE / RS_THREADS; ++i) {
-    int64_t idx = base + static_cast<int64_t>(i) * RS_THREADS + threadIdx.x;
+  // all of this thread's keys in flight first (the loop below is latency
+  // bound otherwise), then warp-aggregated shared-memory counts
+  constexpr int PER = RS_TILE / RS_THREADS;
+  uint64_t k[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int64_t idx = base + static_cast<int64_t>(i) * RS_THREADS + threadIdx.x;
+    k[i] = idx < n ? keys[idx] : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int64_t idx = base + static_cast<int64_t>(i) * RS_THREADS + threadIdx.x;
     bool valid = idx < n;
-    unsigned d = valid ? rs_digit(keys[idx], shift, mask) : 0xFFFFu;
+    unsigned d = valid ? rs_digit(k[i], shift, mask) : 0xFFFFu;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     if (valid && lane == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&cnt[d], __popc(peers));
   }

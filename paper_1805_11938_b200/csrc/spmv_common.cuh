@@ -48,13 +48,6 @@ __device__ __forceinline__ void for_each_empty_row(int64_t n_rows, const int32_t
   for_each_empty_row(n_rows, ptr, f, blockIdx.x, gridDim.x);
 }
 
-// Blocks to give an empty-row pass folded into a SpMV kernel's grid (it runs
-// alongside the gather-bound main blocks instead of as its own launch).
-inline int64_t empty_row_blocks(int64_t n_rows, int threads) {
-  const int64_t want = (n_rows + threads * 16 - 1) / (threads * 16);
-  return want < 148 * 2 ? want : 148 * 2;
-}
-
 // Folds chains of equal non-negative keys over items [begin, end): a chain is
 // a maximal run of consecutive items with the same key; apply(key, sum) gets
 // the chain's sum.  The sum is defined independently of how items map to
@@ -99,12 +92,22 @@ __device__ __forceinline__ void fold_chains(int64_t begin, int64_t end, Key key_
       longs &= longs - 1;
       const int32_t k = __shfl_sync(0xffffffffu, r, l);
       double acc = 0.0;
-      for (int64_t b = w0 + l;; b += 32) {
-        const int64_t tt = b + lane;
-        const unsigned m = __ballot_sync(0xffffffffu, key(tt) == k);
-        const int n = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
-        if (lane < n) acc += val_of(tt);
-        if (n < 32) break;
+      bool done = false;
+      for (int64_t b = w0 + l; !done; b += 4 * 32) {  // four 32-item blocks per round trip
+        bool in[4];
+        double cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) in[u] = key(b + u * 32 + lane) == k;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cv[u] = in[u] ? val_of(b + u * 32 + lane) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (done) break;
+          const unsigned m = __ballot_sync(0xffffffffu, in[u]);
+          const int n = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+          if (lane < n) acc += cv[u];
+          done = n < 32;
+        }
       }
       acc = warp_sum(acc);
       if (lane == 0) apply(k, acc);

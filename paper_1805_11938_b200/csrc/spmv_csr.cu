@@ -68,23 +68,23 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     const double* __restrict__ val, const int32_t* __restrict__ nz_rows, const int32_t* __restrict__ chunk_row,
     int64_t nchunks, int32_t* __restrict__ carry_row, double* __restrict__ carry_val, const double* __restrict__ x,
     double* __restrict__ y, const double* __restrict__ scale_p, int64_t ell_k, const int32_t* __restrict__ ell_idx,
-    const double* __restrict__ ell_val, int64_t empty_blocks) {
+    const double* __restrict__ ell_val, int64_t rows_per_block) {
   static_assert(S == 8, "lane-contiguous loads assume 8 entries (32 B of indices) per lane");
   constexpr int CH = 32 * S;
-  if (blockIdx.x < empty_blocks) {
-    // empty rows (HYB: rows whose tail is empty get their ELL part), beside
-    // the gather-bound chunk blocks instead of as a separate launch
+  if (rows_per_block > 0) {
+    // this block's slice of the empty rows (HYB: rows whose tail is empty get
+    // their ELL part), riding along with the gather-bound chunk work
     const double sc = load_scale(scale_p);
-    for_each_empty_row(
-        n_rows, ptr,
-        [&](int64_t r) { y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0; },
-        blockIdx.x, empty_blocks);
-    return;
+    const int64_t r0 = blockIdx.x * rows_per_block;
+    const int64_t r1 = r0 + rows_per_block < n_rows ? r0 + rows_per_block : n_rows;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+      if (ld_stream(ptr + r) == ld_stream(ptr + r + 1))
+        y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem<S>& sm = *reinterpret_cast<ChunkSmem<S>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = static_cast<int64_t>(blockIdx.x - empty_blocks) * CK_WARPS + w;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * CK_WARPS + w;
   if (c >= nchunks) return;  // whole warps only
   const int64_t k0 = c * CH;
   const int cnt = static_cast<int>(nnz - k0 < CH ? nnz - k0 : CH);
@@ -215,12 +215,13 @@ struct ChunkArgs {
 };
 
 template <int S, bool HAS_ELL, bool VEC>
-void launch_main(const ChunkArgs& a, int64_t nchunks, int64_t empty_blocks, cudaStream_t s) {
+void launch_main(const ChunkArgs& a, int64_t nchunks, bool empties, cudaStream_t s) {
   const size_t smem = sizeof(ChunkSmem<S>);
-  k_spmv_chunk<S, HAS_ELL, VEC>
-      <<<static_cast<unsigned>(empty_blocks + (nchunks + CK_WARPS - 1) / CK_WARPS), CK_WARPS * 32, smem, s>>>(
-          a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x, a.y,
-          a.scale, a.ell_k, a.ell_idx, a.ell_val, empty_blocks);
+  const int64_t blocks = (nchunks + CK_WARPS - 1) / CK_WARPS;
+  const int64_t rpb = empties ? (a.n_rows + blocks - 1) / blocks : 0;
+  k_spmv_chunk<S, HAS_ELL, VEC><<<static_cast<unsigned>(blocks), CK_WARPS * 32, smem, s>>>(
+      a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x, a.y,
+      a.scale, a.ell_k, a.ell_idx, a.ell_val, rpb);
   SPMVB_LAUNCHED("k_spmv_chunk");
 }
 
@@ -237,12 +238,11 @@ void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
     }
     return;
   }
-  const int64_t eb = empties ? empty_row_blocks(a.n_rows, CK_WARPS * 32) : 0;
   // 256-bit loads need 32-byte aligned index/value arrays (torch allocations are)
-  if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, eb, s);
-  else launch_main<S, HAS_ELL, false>(a, nchunks, eb, s);
+  if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, empties, s);
+  else launch_main<S, HAS_ELL, false>(a, nchunks, empties, s);
   if (nchunks > 1) {
-    k_chunk_fixup<<<grid_for(nchunks, 256, 148 * 8), 256, 0, s>>>(nchunks, a.carry_row, a.carry_val, a.y, a.scale);
+    k_chunk_fixup<<<grid_for(nchunks, 256), 256, 0, s>>>(nchunks, a.carry_row, a.carry_val, a.y, a.scale);
     SPMVB_LAUNCHED("k_chunk_fixup");
   }
 }

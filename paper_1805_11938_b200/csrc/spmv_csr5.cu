@@ -144,21 +144,22 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
 // warp keeps 32*S gathers in flight (random-column matrices are bound by the
 // L1TEX rate of these gathers, ~1 distinct line per SM cycle).  The trailing
 // partial tile (row-major over its occupied cells, formats.py:24-25) takes a
-// different load path in the same kernel.  The first `empty_blocks` blocks
-// instead zero the empty rows of [row_begin, row_end): that streaming pass
-// runs beside the gather-bound tile blocks rather than as its own launch.
+// different load path in the same kernel.  Every block also zeroes its share
+// of the empty rows of [row_begin, row_end) (a coalesced slice of ptr/y per
+// block), so that streaming pass rides along with the gather-bound tiles
+// instead of costing its own launch.
 template <int W, int S>
 __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
-                                                     int64_t empty_blocks, int64_t row_begin, int64_t row_end) {
-  if (blockIdx.x < empty_blocks) {
-    double* yb = C.y + row_begin;
-    for_each_empty_row(row_end - row_begin, C.ptr + row_begin, [&](int64_t r) { yb[r] = 0.0; }, blockIdx.x,
-                       empty_blocks);
-    return;
+                                                     int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
+  if (rows_per_block > 0) {
+    const int64_t r0 = row_begin + blockIdx.x * rows_per_block;
+    const int64_t r1 = r0 + rows_per_block < row_end ? r0 + rows_per_block : row_end;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+      if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
   }
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
-  const int64_t group = t_begin + ((blockIdx.x - empty_blocks) * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
+  const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
   const bool active = group < t_end;
   const int64_t t = active ? group : t_begin;
   const int64_t tile0 = t * static_cast<int64_t>(W) * S;
@@ -244,9 +245,17 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
 // continues the same row) inside [t_begin, t_end), chain by chain in tile
 // order (fold_chains); the carries are already scaled.
 __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __restrict__ tile_ptr,
-                             const uint32_t* __restrict__ aux, const double* __restrict__ carry, double* __restrict__ y) {
+                             const uint32_t* __restrict__ aux, const double* __restrict__ carry,
+                             double* __restrict__ y) {
+  // chain key = the continued row, tile_ptr[t] (coalesced, loaded alongside
+  // aux[t] rather than after it)
   fold_chains(
-      t_begin, t_end, [&](int64_t t) -> int32_t { return (aux[t] & 0x80000000u) ? tile_ptr[t] : -1; },
+      t_begin, t_end,
+      [&](int64_t t) -> int32_t {
+        const uint32_t a = aux[t];
+        const int32_t r = tile_ptr[t];
+        return (a & 0x80000000u) ? r : -1;
+      },
       [&](int64_t t) { return carry[t]; }, [&](int32_t r, double acc) { y[r] = y[r] + acc; });
 }
 
@@ -281,9 +290,9 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
     }
   };
   auto warp_s_launch = [&](auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
-    const int64_t eb = empties ? empty_row_blocks(row_end - row_begin, 256) : 0;
-    kern<<<static_cast<unsigned>(eb + (t_end - t_begin) * W / 256 + ((t_end - t_begin) * W % 256 ? 1 : 0)), 256, 0,
-           s>>>(C, t_begin, t_end, eb, row_begin, row_end);
+    const int64_t blocks = ((t_end - t_begin) * W + 255) / 256;
+    const int64_t rpb = empties ? (row_end - row_begin + blocks - 1) / blocks : 0;
+    kern<<<static_cast<unsigned>(blocks), 256, 0, s>>>(C, t_begin, t_end, rpb, row_begin, row_end);
     SPMVB_LAUNCHED("k_csr5_warp_s");
     generic_begin = t_end;
   };
@@ -320,8 +329,8 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
     SPMVB_LAUNCHED("k_csr5_generic");
   }
   if (t_end - t_begin > 1 || t_begin > 0) {
-    k_csr5_fixup<<<grid_for(t_end - t_begin, 256, 148 * 8), 256, 0, s>>>(t_begin, t_end, C.tile_ptr, C.aux, C.carry,
-                                                                         C.y);
+    // one 32-tile window per warp: every window's loads are in flight at once
+    k_csr5_fixup<<<grid_for(t_end - t_begin, 256), 256, 0, s>>>(t_begin, t_end, C.tile_ptr, C.aux, C.carry, C.y);
     SPMVB_LAUNCHED("k_csr5_fixup");
   }
 }

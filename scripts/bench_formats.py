@@ -4,7 +4,7 @@
 
 For every BASELINE.json config C1-C4 and every format (reference default
 parameters AND the GPU-tuned ones) it times y = A x with CUDA events, flushing
-L2 (a 512 MB write) before every rep so the number is an HBM number; it also
+L2 (a 512 MB read) before every rep so the number is an HBM number; it also
 reports the hot (no-flush) time.  Algorithmic bytes = the reference byte
 model (harness.spmv_bytes); GFLOP/s = 2 nnz / t.  Each record also holds the
 conversion time and a parity check against dense_spmv_oracle on the device
@@ -49,12 +49,14 @@ def build(name):
 def timed(fn, reps, flush):
     """Median device time of fn(); all reps are enqueued before one sync so
     the host runs ahead (the 512 MB flush in front of each rep hides the
-    host-side launch cost)."""
+    host-side launch cost).  The flush READS 512 MB, so L2 is left holding
+    clean foreign lines: a write flush would leave ~126 MB of dirty lines
+    whose write-back would be charged to the kernel."""
     evs = []
     torch.cuda.synchronize()
     for _ in range(reps):
         if flush is not None:
-            flush.zero_()
+            flush.sum()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         fn()
@@ -97,7 +99,7 @@ def main():
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.zeros(64 << 20, dtype=torch.float64, device="cuda")  # 512 MB, read before each cold rep
     out = open(args.out, "w") if args.out else None
     for name in args.configs.split(","):
         a = build(name)
