@@ -167,16 +167,21 @@ __device__ __forceinline__ double seq_slots(int64_t k, int64_t stride, int64_t b
 
 // The same recurrence four slots at a time without the prefetch: fewer
 // registers, so more resident threads -- better for short rows (k <= 8).
+// CACHED: slot loads through L1 (narrow SELL slices: the 16-byte index pieces
+// of consecutive slots share 32-byte sectors, which L1 then serves).
+template <bool CACHED = false>
 __device__ __forceinline__ double seq_slots4(int64_t k, int64_t stride, int64_t base, const int32_t* __restrict__ idx,
                                              const double* __restrict__ val, const double* __restrict__ x) {
+  auto li = [](const int32_t* p) { return CACHED ? __ldg(p) : ld_stream(p); };
+  auto lv = [](const double* p) { return CACHED ? __ldg(p) : ld_stream(p); };
   double acc = 0.0;
   int64_t j = 0;
   for (; j + 4 <= k; j += 4) {
     const int64_t o = base + j * stride;
-    const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + stride);
-    const double v2 = ld_stream(val + o + 2 * stride), v3 = ld_stream(val + o + 3 * stride);
-    const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + stride);
-    const int32_t c2 = ld_stream(idx + o + 2 * stride), c3 = ld_stream(idx + o + 3 * stride);
+    const double v0 = lv(val + o), v1 = lv(val + o + stride);
+    const double v2 = lv(val + o + 2 * stride), v3 = lv(val + o + 3 * stride);
+    const int32_t c0 = li(idx + o), c1 = li(idx + o + stride);
+    const int32_t c2 = li(idx + o + 2 * stride), c3 = li(idx + o + 3 * stride);
     acc = __dadd_rn(acc, __dmul_rn(v0, ldx(x, c0)));
     acc = __dadd_rn(acc, __dmul_rn(v1, ldx(x, c1)));
     acc = __dadd_rn(acc, __dmul_rn(v2, ldx(x, c2)));
@@ -184,7 +189,7 @@ __device__ __forceinline__ double seq_slots4(int64_t k, int64_t stride, int64_t 
   }
   for (; j < k; ++j) {
     const int64_t o = base + j * stride;
-    acc = __dadd_rn(acc, __dmul_rn(ld_stream(val + o), ldx(x, ld_stream(idx + o))));
+    acc = __dadd_rn(acc, __dmul_rn(lv(val + o), ldx(x, li(idx + o))));
   }
   return acc;
 }

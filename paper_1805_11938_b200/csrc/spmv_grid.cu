@@ -24,18 +24,25 @@ __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict_
 }
 
 // =============================================================== SELL ====
-__global__ void k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
+// MODE 0: four slots per step; 1: the same through L1 (c < 8); 2: with the
+// next four slots prefetched (rows longer than 8 slots).
+template <int MODE>
+__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE == 2 ? 5 : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
   const double s = load_scale(scale_p);
+  const int32_t c32 = static_cast<int32_t>(c);  // n_rows < 2^31: 32-bit slice arithmetic
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n_rows;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t sl = p / c, local = p - sl * c;
-    const int64_t rows_s = (sl + 1) * c <= n_rows ? c : n_rows - sl * c;
+    const int32_t p32 = static_cast<int32_t>(p);
+    const int32_t sl = p32 / c32, local = p32 - sl * c32;
+    const int64_t rows_s = (static_cast<int64_t>(sl) + 1) * c <= n_rows ? c : n_rows - static_cast<int64_t>(sl) * c;
     const int64_t w = widths[sl];
     if (w > SPMVB_SELL_WIDE_COLS && rows_s <= 128) continue;  // k_spmv_sell_wide's slice
-    const double acc = seq_slots4(w, rows_s, slice_off[sl] + local, idx, val, x);
+    const int64_t base = slice_off[sl] + local;
+    const double acc = MODE == 2 ? seq_slots(w, rows_s, base, idx, val, x)
+                                 : seq_slots4<MODE == 1>(w, rows_s, base, idx, val, x);
     const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
     y[r] = scale_p ? s * acc : acc;
   }
@@ -103,10 +110,11 @@ __global__ void k_sell_mark_wide(const int64_t* __restrict__ widths, int64_t n_r
 }  // namespace
 
 extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out,
-                                    int64_t* n_wide, void* stream) {
+                                    int64_t* n_wide, int64_t* max_narrow_width, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     *n_wide = 0;
+    if (max_narrow_width) *max_narrow_width = 0;
     if (n_rows <= 0 || c < 1) return;
     const int64_t n_slices = (n_rows + c - 1) / c;
     DevBuf<uint8_t> flag(n_slices, s);
@@ -123,6 +131,13 @@ extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* wi
     int32_t h = 0;
     copy_to_host(&h, total.get(), 1, s);
     *n_wide = h;
+    if (max_narrow_width) {
+      DevBuf<int64_t> mx(1, s);
+      device_reduce<int64_t>(
+          n_slices, [=] __device__(int64_t i) -> int64_t { return f[i] ? 0 : widths[i]; }, OpMax{}, int64_t{0},
+          mx.get(), s);
+      copy_to_host(max_narrow_width, mx.get(), 1, s);
+    }
   });
 }
 
@@ -139,11 +154,18 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
 
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
-                               int64_t n_wide, const double* x, double* y, const double* scale, void* stream) {
+                               int64_t n_wide, int64_t max_narrow_width, const double* x, double* y,
+                               const double* scale, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
-    k_spmv_sell<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
+    // c < 8: slot loads through L1 (the other half of each index sector is
+    // the next slot's); wide rows (> 8 slots): next four slots prefetched
+    const unsigned g = grid_for(n_rows, 256);
+    if (c < 8) k_spmv_sell<1><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
+    else if (max_narrow_width > 8 || max_narrow_width < 0)
+      k_spmv_sell<2><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
+    else k_spmv_sell<0><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_sell");
     if (n_wide > 0) {
       k_spmv_sell_wide<<<static_cast<unsigned>(n_wide), 256, 0, s>>>(n_rows, c, wide, widths, slice_off, perm, idx,

@@ -275,15 +275,17 @@ class SellMatrix:
         self._wide = None
 
     def wide_plan(self):
-        """Slices wider than SPMVB_SELL_WIDE_COLS (kernel-side, built once)."""
+        """(wide slice list, count, widest remaining slice): slices wider than
+        SPMVB_SELL_WIDE_COLS get a CTA each (kernel-side, built once)."""
         if self._wide is None:
             n_slices = self.n_slices
             lst = _i32(max(n_slices, 1), self.device)
             cnt = ctypes.c_int64()
+            mx = ctypes.c_int64()
             with torch.cuda.device(self.device):
                 check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), ptr(lst), ctypes.byref(cnt),
-                                               _lib.stream(self.device)))
-            self._wide = (lst, int(cnt.value))
+                                               ctypes.byref(mx), _lib.stream(self.device)))
+            self._wide = (lst, int(cnt.value), int(mx.value))
         return self._wide
 
     def _host_layout(self):
