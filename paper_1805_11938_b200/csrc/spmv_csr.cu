@@ -91,37 +91,42 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
   int32_t* seg = sm.seg[w];
   uint32_t* flag = sm.flag[w];
 
+  // The chunk's row table first: its loads (chunk_row -> nz_rows -> ptr) are
+  // a dependent chain, issued so that they overlap the value/column loads
+  // and the x gathers instead of following them.
+  const int32_t ia = chunk_row[c], ib = chunk_row[c + 1];
   // 1. lane l owns entries [8l, 8l+8): one 256-bit load of its column
   //    indices and two of its values (full sectors; with the lanes' rows
   //    consecutive, the x gathers of one instruction fall in few lines on
   //    banded/stencil matrices), then 8 independent gathers in flight.
   double v[S];
-  {
-    const int e0 = lane * S;
-    int32_t ci[S];
-    if (VEC && e0 + S <= cnt) {
-      ld_stream8(col + k0 + e0, ci);
-      ld_stream4(val + k0 + e0, v);
-      ld_stream4(val + k0 + e0 + 4, v + 4);
-    } else {
+  int32_t ci[S];
+  const int e0 = lane * S;
+  if (VEC && e0 + S <= cnt) {
+    ld_stream8(col + k0 + e0, ci);
+    ld_stream4(val + k0 + e0, v);
+    ld_stream4(val + k0 + e0 + 4, v + 4);
+  } else {
 #pragma unroll
-      for (int i = 0; i < S; ++i) {
-        const bool ok = e0 + i < cnt;
-        ci[i] = ok ? ld_stream(col + k0 + e0 + i) : 0;
-        v[i] = ok ? ld_stream(val + k0 + e0 + i) : 0.0;
-      }
+    for (int i = 0; i < S; ++i) {
+      const bool ok = e0 + i < cnt;
+      ci[i] = ok ? ld_stream(col + k0 + e0 + i) : 0;
+      v[i] = ok ? ld_stream(val + k0 + e0 + i) : 0.0;
     }
-#pragma unroll
-    for (int i = 0; i < S; ++i) v[i] = e0 + i < cnt ? v[i] * ldx(x, ci[i]) : 0.0;
   }
+  // first batch of row starts (most chunks have at most 32)
+  const int32_t i0 = ia + lane;
+  const int32_t r0 = i0 < ib ? (nz_rows ? nz_rows[i0] : i0) : 0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) v[i] = e0 + i < cnt ? v[i] * ldx(x, ci[i]) : 0.0;
+  const int32_t p0 = i0 < ib ? ptr[r0] : 0;
   if (lane < CH / 32) flag[lane] = 0u;
   __syncwarp();
   // 2. non-empty rows starting in this chunk (at most CH of them)
   const double sc = load_scale(scale_p);
-  const int32_t ia = chunk_row[c], ib = chunk_row[c + 1];
-  for (int32_t i = ia + lane; i < ib; i += 32) {
-    const int32_t r = nz_rows ? nz_rows[i] : i;
-    const int p = static_cast<int>(ptr[r] - k0);
+  for (int32_t i = i0; i < ib; i += 32) {
+    const int32_t r = i == i0 ? r0 : (nz_rows ? nz_rows[i] : i);
+    const int p = static_cast<int>((i == i0 ? p0 : ptr[r]) - k0);
     seg[p] = r;
     atomicOr(&flag[p >> 5], 1u << (p & 31));
     // HYB: the row's ELL part, parked unscaled in y[r] for the lane that
