@@ -306,7 +306,7 @@ def run_ours(args):
     def make_pi(exchange):
         return spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_full, exchange=exchange,
                                      local_cols=shard.indices if exchange == "sparse" else None,
-                                     local_ranges=ranges if exchange == "allgatherv" else None,
+                                     local_ranges=ranges if exchange in ("allgatherv", "p2p") else None,
                                      local_spmv_range=range_fn)
 
     pi = make_pi(args.exchange)
@@ -341,30 +341,38 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_loop = float(tt.item())
     value = 2.0 * nnz * args.steps / t_loop / 1e9
-    exchange = {"mode": pi.exchange, "overlap_ranges": len(ranges) if ranges else 1}
+    exchange = {"mode": pi.exchange, "overlap_ranges": len(ranges) if ranges else 1,
+                f"ms_per_step_{pi.exchange}": t_loop / args.steps * 1e3}
     if world > 1:
-        # the other exchange, same steps, for comparison (report both)
-        other = "allgatherv" if pi.exchange == "sparse" else "sparse"
+        # the other exchanges, same steps, for comparison (report
+        # the all-gather and the sparse exchange; p2p = our kernels over NVLink)
         vol = getattr(pi, "exchange_volume", None)
+        mode = pi.exchange
         del pi
-        pj = make_pi(other)
-        for _ in range(warmup):
-            pj.step()
-        dist.barrier()
-        torch.cuda.synchronize()
-        ev0.record()
-        for _ in range(args.steps):
-            pj.step()
-        ev1.record()
-        torch.cuda.synchronize()
-        tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        vol = vol or getattr(pj, "exchange_volume", None)
-        exchange.update({f"ms_per_step_{pj.exchange}": float(tt.item()) / args.steps * 1e3,
-                         f"ms_per_step_{exchange['mode']}": t_loop / args.steps * 1e3})
+        others = ("allgatherv", "sparse", "p2p") if args.compare_p2p else ("allgatherv", "sparse")
+        for other in others:
+            if other == mode:
+                continue
+            try:
+                pj = make_pi(other)
+                for _ in range(warmup):
+                    pj.step()
+                dist.barrier()
+                torch.cuda.synchronize()
+                ev0.record()
+                for _ in range(args.steps):
+                    pj.step()
+                ev1.record()
+                torch.cuda.synchronize()
+                tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                exchange[f"ms_per_step_{other}"] = float(tt.item()) / args.steps * 1e3
+                vol = vol or getattr(pj, "exchange_volume", None)
+                del pj
+            except Exception as exc:  # e.g. symmetric memory unavailable: report, keep the run
+                exchange[f"error_{other}"] = f"{type(exc).__name__}: {str(exc)[:160]}"
         if vol:
             exchange["rank0_volume_entries"] = vol
-        del pj
 
     # ---- end to end through the public API with host buffers ----
     # (host x in, host y out; the output buffer is the caller's, like numpy's out=)
@@ -445,7 +453,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--overlap-ranges", type=int, default=4,
                     help="N > 1, CSR5 shards: row ranges whose all-gatherv overlaps the remaining local SpMV")
-    ap.add_argument("--exchange", choices=["allgatherv", "sparse"], default="allgatherv",
+    ap.add_argument("--compare-p2p", action="store_true",
+                    help="N > 1: also time the peer-memory exchange (symmetric memory) next to the default")
+    ap.add_argument("--exchange", choices=["allgatherv", "sparse", "p2p"], default="allgatherv",
                     help="x exchange between row blocks (N > 1): the north-star all-gather of x (default), or "
                          "only the entries each shard reads; the other one is timed too and reported")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)

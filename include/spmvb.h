@@ -280,6 +280,17 @@ int spmvb_column_set(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* c
 int spmvb_gather_f64(const double* src, int64_t base, const int32_t* idx, int64_t n, double* dst, void* stream);
 int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream);
 
+/* Peer-memory exchange of the row-block power iteration (dist.py
+ * exchange="p2p"): spmvb_push_rows writes src[0..n) into every peer buffer
+ * dst_ptrs[p] + offset (a device array of n_peers addresses mapped over
+ * NVLink, e.g. symmetric-memory peers; 16-byte stores) -- the all-gather of
+ * x done by our own kernel, one launch per finished row range, overlapping
+ * the next range's SpMV.  spmvb_sum_inv_sqrt folds the ranks' pushed
+ * ||y_p||^2 values in rank order and writes sumsq and 1/sqrt(sumsq). */
+int spmvb_push_rows(const double* src, int64_t n, const uint64_t* dst_ptrs, int n_peers, int64_t offset,
+                    void* stream);
+int spmvb_sum_inv_sqrt(const double* vals, int n, double* sumsq, double* scale, void* stream);
+
 /* Roofline probe (bench.py): partial[t] = sum of src[idx[i]] over thread t's
  * share of [0, n), 16 gathers in flight per thread, no per-element stores --
  * the L1TEX rate of a matrix's x gathers, which its SpMV cannot beat.

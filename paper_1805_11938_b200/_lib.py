@@ -99,6 +99,8 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_column_set": (c_int, [vp, c_i64, c_i64, vp, P_i64, vp]),
     "spmvb_gather_f64": (c_int, [vp, c_i64, vp, c_i64, vp, vp]),
     "spmvb_scatter_f64": (c_int, [vp, vp, c_i64, vp, vp]),
+    "spmvb_push_rows": (c_int, [vp, c_i64, vp, c_int, c_i64, vp]),
+    "spmvb_sum_inv_sqrt": (c_int, [vp, c_int, vp, vp, vp]),
     "spmvb_gather_probe_threads": (c_i64, []),
     "spmvb_gather_probe": (c_int, [vp, vp, c_i64, vp, vp]),
     "spmvb_csr_features": (c_int, [c_i64, c_i64, c_i64, vp, P_dbl, vp]),

@@ -75,6 +75,40 @@ __global__ void k_gather_sum(const double* __restrict__ src, const int32_t* __re
   partial[tid] = acc;
 }
 
+// Rows [0, n) of src written into every peer buffer dst[p] + offset (peer
+// addresses mapped over NVLink, e.g. symmetric-memory buffers): 16-byte
+// vector stores where the alignment allows, one pass over src per launch.
+__global__ void k_push_rows(const double* __restrict__ src, int64_t n, const uint64_t* __restrict__ dst, int n_peers,
+                            int64_t offset) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // head element when offset is odd (peer buffers are 16-byte aligned)
+  const int64_t head = (offset & 1) ? 1 : 0;
+  if (head && tid == 0 && n > 0)
+    for (int p = 0; p < n_peers; ++p) reinterpret_cast<double*>(dst[p])[offset] = src[0];
+  const int64_t pairs = (n - head) / 2;
+  for (int64_t i = tid; i < pairs; i += stride) {
+    const int64_t e = head + 2 * i;
+    const double a = src[e], b = src[e + 1];
+    for (int p = 0; p < n_peers; ++p) {
+      double2* d = reinterpret_cast<double2*>(reinterpret_cast<double*>(dst[p]) + offset + e);
+      *d = make_double2(a, b);
+    }
+  }
+  const int64_t last = head + 2 * pairs;
+  if (last < n && tid == 0)
+    for (int p = 0; p < n_peers; ++p) reinterpret_cast<double*>(dst[p])[offset + last] = src[last];
+}
+
+// sumsq = vals[0] + vals[1] + ... (rank order), scale = 1/sqrt(sumsq).
+__global__ void k_sum_inv_sqrt(const double* __restrict__ vals, int n, double* __restrict__ sumsq,
+                               double* __restrict__ scale) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += vals[i];
+  *sumsq = s;
+  *scale = 1.0 / sqrt(s);
+}
+
 }  // namespace
 
 extern "C" int spmvb_column_set(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* cols_out, int64_t* n_out,
@@ -127,5 +161,25 @@ extern "C" int spmvb_gather_probe(const double* src, const int32_t* idx, int64_t
     cudaStream_t s = as_stream(stream);
     k_gather_sum<<<148 * 8, 256, 0, s>>>(src, idx, n, partial);
     SPMVB_LAUNCHED("k_gather_sum");
+  });
+}
+
+extern "C" int spmvb_push_rows(const double* src, int64_t n, const uint64_t* dst_ptrs, int n_peers, int64_t offset,
+                               void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n <= 0 || n_peers <= 0) return;
+    if (!dst_ptrs) fail(SPMVB_INVALID_ARG, "dst_ptrs is required");
+    k_push_rows<<<grid_for((n + 1) / 2, 256, 148 * 8), 256, 0, s>>>(src, n, dst_ptrs, n_peers, offset);
+    SPMVB_LAUNCHED("k_push_rows");
+  });
+}
+
+extern "C" int spmvb_sum_inv_sqrt(const double* vals, int n, double* sumsq, double* scale, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n < 1) fail(SPMVB_INVALID_ARG, "n must be >= 1");
+    k_sum_inv_sqrt<<<1, 1, 0, s>>>(vals, n, sumsq, scale);
+    SPMVB_LAUNCHED("k_sum_inv_sqrt");
   });
 }

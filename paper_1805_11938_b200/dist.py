@@ -16,6 +16,13 @@ SpMV by linearity.  The local SpMV writes straight into this rank's slice
 of the next x (no copy).  The same code runs over gloo with CPU tensors in
 the tests (the local SpMV is injectable).
 
+``exchange="p2p"`` does the all-gather with our own kernel over peer
+memory instead of NCCL: x lives in symmetric memory mapped into every rank,
+each finished row range is stored straight into the peers' next iterate
+(overlapping the next range's SpMV), the per-rank ||y_p||^2 go into the
+peers' norm slots, and one device-side barrier ends the step (no host
+round trip, no NCCL).
+
 ``exchange="sparse"`` replaces the all-gatherv by the exchange of only the
 x entries each shard's columns touch (§8(e): ~20% of the columns per shard
 at C4, so ~4-5x less traffic): the column sets and the per-peer request
@@ -122,7 +129,7 @@ class PowerIteration:
     def __init__(self, local_spmv: Callable, bounds, rank: int, world: int, device: torch.device,
                  x0: torch.Tensor, group=None, ops=None, exchange: str = "allgatherv",
                  local_cols: torch.Tensor | None = None, local_ranges=None, local_spmv_range: Callable | None = None):
-        if exchange not in ("allgatherv", "sparse"):
+        if exchange not in ("allgatherv", "sparse", "p2p"):
             raise ValueError(f"unknown exchange {exchange!r}")
         self.local_spmv = local_spmv
         self.bounds = [int(b) for b in bounds]
@@ -136,7 +143,13 @@ class PowerIteration:
         self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
         self.scale = torch.ones(1, dtype=torch.float64, device=device)
         self.lo, self.hi = self.bounds[rank], self.bounds[rank + 1]
-        self.exchange = exchange if world > 1 else "allgatherv"
+        # p2p also runs at world 1 (no peers: it exercises the buffers,
+        # barrier and norm slots on one GPU)
+        self.exchange = exchange if (world > 1 or exchange == "p2p") else "allgatherv"
+        self._ranges_local = local_ranges
+        self.local_spmv_range = local_spmv_range
+        if self.exchange == "p2p":
+            self._plan_p2p(x0, n)
         if self.exchange == "sparse":
             if local_cols is None:
                 raise ValueError("exchange='sparse' needs local_cols (the shard's column indices)")
@@ -153,7 +166,6 @@ class PowerIteration:
             allspans = [None] * world
             dist.all_gather_object(allspans, spans, group=self.group)
             self._spans = allspans
-            self.local_spmv_range = local_spmv_range
 
     # ---- full exchange ---------------------------------------------------
     def _allgatherv(self, y_full: torch.Tensor) -> None:
@@ -259,7 +271,84 @@ class PowerIteration:
         self.ops.inv_sqrt(self.sumsq, self.scale)
         self.x, self.x_next = self.x_next, self.x
 
+    # ---- peer-memory exchange (our kernels over NVLink, no NCCL) ----------
+    def _plan_p2p(self, x0: torch.Tensor, n: int) -> None:
+        """x / x_next live in symmetric memory mapped into every rank; each
+        step pushes this rank's rows straight into the peers' next iterate
+        (spmvb_push_rows, one launch per finished row range on a side stream,
+        overlapping the next range) and its ||y_p||^2 into their norm slots,
+        then one device-side barrier ends the step.  Norm slots alternate
+        between two halves by step parity, and a rank writes a peer's x only
+        after the barrier that ends the peer's reads of it."""
+        import torch.distributed._symmetric_memory as symm
+
+        group = self.group if self.group is not None else dist.group.WORLD
+        P, me, dev = self.world, self.rank, self.device
+        self._bufs, self._handles, self._peer_ptrs = [], [], []
+        for _ in range(2):
+            b = symm.empty(max(n, 1), dtype=torch.float64, device=dev)
+            h = symm.rendezvous(b, group)
+            peers = [int(h.buffer_ptrs[q]) + int(h.offset) for q in range(P) if q != me]
+            self._bufs.append(b)
+            self._handles.append(h)
+            self._peer_ptrs.append(torch.tensor(peers or [0], dtype=torch.int64, device=dev))
+        if self._handles[0].buffer_ptrs[me] + self._handles[0].offset != self._bufs[0].data_ptr():
+            raise RuntimeError("symmetric-memory peer addressing does not match the local buffer")
+        self._sums = symm.empty(2 * P, dtype=torch.float64, device=dev)
+        self._sums_h = symm.rendezvous(self._sums, group)
+        self._sums_peers = torch.tensor(
+            [int(self._sums_h.buffer_ptrs[q]) + int(self._sums_h.offset) for q in range(P) if q != me] or [0],
+            dtype=torch.int64, device=dev)
+        self._bufs[0][:n].copy_(x0.to(device=dev, dtype=torch.float64))
+        self.x, self.x_next = self._bufs[0][:n], self._bufs[1][:n]
+        self._cur = 0  # index of the buffer holding x
+        self._parity = 0
+        self._push_stream = torch.cuda.Stream(device=dev)
+
+    def _push(self, buf_index: int, a: int, b: int) -> None:
+        """Rows [a, b) (global) of buffer `buf_index` into the same rows of every peer's buffer."""
+        if b <= a or self.world == 1:
+            return
+        src = self._bufs[buf_index][a:b]
+        with torch.cuda.device(self.device):
+            check(LIB.spmvb_push_rows(ptr(src), b - a, self._peer_ptrs[buf_index].data_ptr(), self.world - 1, a,
+                                      _lib.stream(self.device)))
+
+    def _step_p2p(self) -> None:
+        nxt = 1 - self._cur
+        out = self.x_next[self.lo : self.hi]
+        main = torch.cuda.current_stream(self.device)
+        if self._ranges_local is not None and self.local_spmv_range is not None:
+            for k, (a, b) in enumerate(self._ranges_local):
+                self.local_spmv_range(k, self.x, out, self.scale)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                self._push_stream.wait_event(ev)
+                with torch.cuda.stream(self._push_stream):
+                    self._push(nxt, self.lo + a, self.lo + b)
+            main.wait_stream(self._push_stream)
+        else:
+            self.local_spmv(self.x, out, self.scale)
+            self._push(nxt, self.lo, self.hi)
+        P, me = self.world, self.rank
+        slot = self._parity * P + me
+        self.ops.sumsq(out, self._sums[slot : slot + 1])
+        if P > 1:
+            with torch.cuda.device(self.device):
+                check(LIB.spmvb_push_rows(ptr(self._sums[slot : slot + 1]), 1, self._sums_peers.data_ptr(), P - 1,
+                                          slot, _lib.stream(self.device)))
+        self._sums_h.barrier(channel=0)
+        half = self._sums[self._parity * P : self._parity * P + P]
+        with torch.cuda.device(self.device):
+            check(LIB.spmvb_sum_inv_sqrt(ptr(half), P, ptr(self.sumsq), ptr(self.scale), _lib.stream(self.device)))
+        self._parity ^= 1
+        self._cur = nxt
+        self.x, self.x_next = self.x_next, self.x
+
     def step(self) -> None:
+        if self.exchange == "p2p":
+            self._step_p2p()
+            return
         if self._spans is not None:
             self._step_overlapped()
             return

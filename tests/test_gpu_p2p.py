@@ -1,0 +1,91 @@
+"""Peer-memory exchange on one GPU: the push kernel against local stand-in
+"peer" buffers (every alignment of offset and length), and the whole
+exchange="p2p" power-iteration step (symmetric memory, device barrier, norm
+slots) at world size 1 against the plain iteration.  Multi-rank runs need
+more GPUs than this harness has; the rank-to-rank ordering argument is in
+dist.PowerIteration._plan_p2p."""
+
+from __future__ import annotations
+
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def sp():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1805_11938_b200 as sp
+
+    return sp
+
+
+def test_push_rows_to_local_peers(sp, rng):
+    from paper_1805_11938_b200 import _lib
+
+    n = 1000
+    src_full = torch.from_numpy(rng.normal(size=n)).cuda()
+    peers = [torch.full((n,), -7.0, dtype=torch.float64, device="cuda") for _ in range(3)]
+    ptrs = torch.tensor([p.data_ptr() for p in peers], dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    for a, b in [(0, 1000), (1, 2), (3, 10), (10, 11), (5, 5), (2, 999), (999, 1000)]:
+        for p in peers:
+            p.fill_(-7.0)
+        _lib.check(_lib.load().spmvb_push_rows(src_full[a:].data_ptr(), b - a, ptrs.data_ptr(), 3, a, stream))
+        want = np.full(n, -7.0)
+        want[a:b] = src_full.cpu().numpy()[a:b]
+        for p in peers:
+            assert np.array_equal(p.cpu().numpy(), want), (a, b)
+
+
+def test_p2p_power_iteration_world1(sp, rng):
+    import torch.distributed as dist
+
+    from paper_1805_11938_b200 import dist as spdist
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    r, c, v = sp.synth.rmat_triplets(scale=12, edge_factor=8, seed=5)
+    n = 1 << 12
+    a = sp.canonicalize(r, c, v, n, n)
+    m = sp.to_csr5(a, 32, 16)
+    x0 = torch.from_numpy(rng.uniform(0.5, 1.0, size=n)).cuda()
+
+    def local(xv, out, scale):
+        sp.spmv("csr5", m, xv, out=out, scale=scale)
+
+    tb, rb = m.range_plan(4)
+    plan = [(int(rb[k]), int(rb[k + 1]) if k + 1 < len(tb) - 1 else n, int(tb[k]), int(tb[k + 1]))
+            for k in range(len(tb) - 1)][::-1]
+
+    def range_fn(k, xv, out, scale):
+        a0, b0, t0, t1 = plan[k]
+        sp.spmv_csr5_tiles(m, xv, out, t0, t1, a0, b0, scale=scale)
+
+    ref = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0)
+    p2p = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0, exchange="p2p")
+    p2r = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0, exchange="p2p",
+                                local_ranges=[(a0, b0) for a0, b0, _, _ in plan], local_spmv_range=range_fn)
+    assert p2p.exchange == "p2p"
+    for _ in range(7):
+        ref.step()
+        p2p.step()
+        p2r.step()
+    torch.cuda.synchronize()
+    want = ref.x.cpu().numpy()
+    for pi in (p2p, p2r):
+        got = pi.gather_full().cpu().numpy()
+        np.testing.assert_allclose(got, want, rtol=1e-14, atol=0)
+        assert float(pi.scale.item()) == pytest.approx(float(ref.scale.item()), rel=1e-14)
