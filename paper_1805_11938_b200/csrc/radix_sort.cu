@@ -7,6 +7,21 @@ __device__ __forceinline__ unsigned rs_digit(uint64_t key, int shift, unsigned m
   return static_cast<unsigned>(key >> shift) & mask;
 }
 
+// Lanes of the warp holding the same digit (warp multi-split by ballots: one
+// ballot per digit bit, constant time however many distinct digits the warp
+// holds -- __match_any_sync slows down with every distinct value).  Only
+// meaningful for valid lanes; invalid lanes are excluded from every mask.
+__device__ __forceinline__ unsigned rs_peers(unsigned d, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {  // RS_RADIX = 256: 8 digit bits
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
 // Per-tile digit histogram, written digit-major: hist[d * num_tiles + tile].
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
                                                         unsigned mask, uint32_t* __restrict__ hist,
@@ -29,8 +44,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
   for (int i = 0; i < PER; ++i) {
     const int64_t idx = base + static_cast<int64_t>(i) * RS_THREADS + threadIdx.x;
     bool valid = idx < n;
-    unsigned d = valid ? rs_digit(k[i], shift, mask) : 0xFFFFu;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned d = valid ? rs_digit(k[i], shift, mask) : 0u;
+    unsigned peers = rs_peers(d, valid);
     if (valid && lane == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&cnt[d], __popc(peers));
   }
   __syncthreads();
@@ -74,8 +89,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __res
   for (int r = 0; r < RS_LANE_ITEMS; ++r) {
     int64_t idx = warp_base + r * 32 + lane;
     bool valid = idx < n;
-    unsigned d = valid ? rs_digit(key[r], shift, mask) : 0xFFFFu;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned d = valid ? rs_digit(key[r], shift, mask) : 0u;
+    unsigned peers = rs_peers(d, valid);
     uint32_t before = 0;
     if (valid) before = sm.wcnt[warp][d];
     __syncwarp();
