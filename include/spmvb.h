@@ -204,9 +204,13 @@ int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const doub
                    double* y, const double* scale, void* stream);
 
 /* spmv_csr5 (kernels.py:139-174). nonempty_rows may be NULL when every row is
- * non-empty. carry: num_tiles scratch doubles. */
+ * non-empty. carry: num_tiles scratch doubles.  flag_bits (may be NULL) is
+ * bit_flag packed one bit per entry (spmvb_csr5_pack_flags): the tile kernel
+ * then reads 64 bytes of flags per 512-entry tile instead of 512. */
+int spmvb_csr5_pack_flags(int64_t nnz, const uint8_t* bit_flag, uint32_t* flag_bits, void* stream);
 int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma, const int32_t* tile_ptr,
-                    const uint8_t* bit_flag, const int32_t* col, const double* val, const uint32_t* tile_aux,
+                    const uint8_t* bit_flag, const uint32_t* flag_bits, const int32_t* col, const double* val,
+                    const uint32_t* tile_aux,
                     const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x, double* y,
                     const double* scale, void* stream);
 
@@ -217,7 +221,8 @@ int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, 
  * after range k -- the multi-GPU power iteration sends them to the peers
  * while the next range computes.  Bit-identical to spmvb_spmv_csr5. */
 int spmvb_spmv_csr5_tiles(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
-                          const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col, const double* val,
+                          const int32_t* tile_ptr, const uint8_t* bit_flag, const uint32_t* flag_bits,
+                          const int32_t* col, const double* val,
                           const uint32_t* tile_aux, const int32_t* nonempty_rows, int64_t n_nonempty, double* carry,
                           const double* x, double* y, const double* scale, int64_t t_begin, int64_t t_end,
                           int64_t row_begin, int64_t row_end, void* stream);
@@ -237,7 +242,8 @@ int spmvb_csr5_range_bounds(int64_t nnz, int omega, int sigma, const int32_t* ti
  * Bit-identical to spmvb_spmv_csr5 on the same inputs.  Pinned host buffers
  * make the copies asynchronous; pageable ones are still correct. */
 int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* ptr, int omega, int sigma,
-                         const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col, const double* val,
+                         const int32_t* tile_ptr, const uint8_t* bit_flag, const uint32_t* flag_bits,
+                         const int32_t* col, const double* val,
                          const uint32_t* tile_aux, const int32_t* nonempty_rows, int64_t n_nonempty, double* carry,
                          const double* x_host, double* x_dev, double* y_dev, double* y_host, const double* scale,
                          int n_ranges, const int64_t* tile_bounds, const int64_t* row_bounds, void* stream);

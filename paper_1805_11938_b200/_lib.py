@@ -76,19 +76,20 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp],
     ),
+    "spmvb_csr5_pack_flags": (c_int, [c_i64, vp, vp, vp]),
     "spmvb_spmv_csr5": (
         c_int,
-        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
+        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
     ),
     "spmvb_csr5_range_bounds": (c_int, [c_i64, c_int, c_int, vp, vp, c_int, vp, vp, vp]),
     "spmvb_spmv_csr5_tiles": (
         c_int,
-        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, c_i64, c_i64, c_i64, c_i64,
-         vp],
+        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, c_i64, c_i64, c_i64,
+         c_i64, vp],
     ),
     "spmvb_spmv_csr5_host": (
         c_int,
-        [c_i64, c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, c_int,
+        [c_i64, c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, c_int,
          vp, vp, vp],
     ),
     "spmvb_spmv_ell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp]),

@@ -23,6 +23,7 @@ struct Csr5Ctx {
   const int32_t* ptr;
   const int32_t* tile_ptr;
   const uint8_t* bit_flag;
+  const uint32_t* fbits;  // bit_flag packed one bit per entry, or null
   const int32_t* col;
   const double* val;
   const uint32_t* aux;
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
 // block), so that streaming pass rides along with the gather-bound tiles
 // instead of costing its own launch.
 template <int W, int S>
-__global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
+__global__ void __launch_bounds__(256, 4) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
                                                      int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
   if (rows_per_block > 0) {
     const int64_t r0 = row_begin + blockIdx.x * rows_per_block;
@@ -169,11 +170,37 @@ __global__ void __launch_bounds__(256) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin,
   double v[S];
   if (active && tile0 + W * S <= C.nnz) {
     const int64_t base = tile0 + j;
+    if (C.fbits) {
+      // the tile's W*S flag bits: NW words, the same for every lane of the
+      // group (broadcast); entry i of lane j is bit (i*W + j) of the tile
+      constexpr int NW = W * S / 32;
+      int32_t fw[NW];
+      const int32_t* tw = reinterpret_cast<const int32_t*>(C.fbits) + (tile0 >> 5);
+      if constexpr (NW % 8 == 0) {
 #pragma unroll
-    for (int i = 0; i < S; ++i) {
-      fmask |= (C.bit_flag[base + i * W] ? 1u : 0u) << i;
-      cidx[i] = ld_stream(C.col + base + i * W);
-      v[i] = ld_stream(C.val + base + i * W);
+        for (int q = 0; q < NW / 8; ++q) {
+          int32_t tmp[8];
+          ld_stream8(tw + 8 * q, tmp);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) fw[8 * q + u] = tmp[u];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) fw[q] = ld_stream(tw + q);
+      }
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        fmask |= ((static_cast<uint32_t>(fw[(i * W) >> 5]) >> (((i * W) & 31) + j)) & 1u) << i;
+        cidx[i] = ld_stream(C.col + base + i * W);
+        v[i] = ld_stream(C.val + base + i * W);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        fmask |= (C.bit_flag[base + i * W] ? 1u : 0u) << i;
+        cidx[i] = ld_stream(C.col + base + i * W);
+        v[i] = ld_stream(C.val + base + i * W);
+      }
     }
 #pragma unroll
     for (int i = 0; i < S; ++i) v[i] *= ldx(C.x, cidx[i]);
@@ -335,6 +362,19 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
   }
 }
 
+// bit_flag (one byte per stored entry) -> one bit per entry: word w holds
+// entries 32w .. 32w+31 (a warp ballot per word).
+__global__ void k_csr5_pack_flags(int64_t nnz, const uint8_t* __restrict__ flag, uint32_t* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t words = (nnz + 31) / 32;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < words;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t e = w * 32 + lane;
+    const unsigned b = __ballot_sync(0xffffffffu, e < nnz && flag[e] != 0);
+    if (lane == 0) bits[w] = b;
+  }
+}
+
 // First tile at or after `target` whose head starts a row (not a continuation).
 __global__ void k_csr5_range_starts(int64_t num_tiles, const uint32_t* __restrict__ aux, int n_ranges,
                                     int64_t* __restrict__ bounds) {
@@ -365,7 +405,8 @@ cudaStream_t copy_stream(int dev) {
 }  // namespace
 
 extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
-                               const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col, const double* val,
+                               const int32_t* tile_ptr, const uint8_t* bit_flag, const uint32_t* flag_bits,
+                               const int32_t* col, const double* val,
                                const uint32_t* tile_aux, const int32_t* nonempty_rows, int64_t n_nonempty,
                                double* carry, const double* x, double* y, const double* scale, void* stream) {
   return guard([&] {
@@ -376,7 +417,7 @@ extern "C" int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, 
       return;
     }
     if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
-    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, col, val, tile_aux,
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, flag_bits, col, val, tile_aux,
               nonempty_rows, carry, x, y, scale};
     const int64_t tile = static_cast<int64_t>(omega) * sigma;
     launch_range(C, 0, (nnz + tile - 1) / tile, 0, n_rows, s);
@@ -415,7 +456,8 @@ extern "C" int spmvb_csr5_range_bounds(int64_t nnz, int omega, int sigma, const 
 }
 
 extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* ptr, int omega,
-                                    int sigma, const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col,
+                                    int sigma, const int32_t* tile_ptr, const uint8_t* bit_flag,
+                                    const uint32_t* flag_bits, const int32_t* col,
                                     const double* val, const uint32_t* tile_aux, const int32_t* nonempty_rows,
                                     int64_t n_nonempty, double* carry, const double* x_host, double* x_dev,
                                     double* y_dev, double* y_host, const double* scale, int n_ranges,
@@ -442,7 +484,7 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
     int dev = 0;
     SPMVB_CUDA(cudaGetDevice(&dev));
     cudaStream_t cs = copy_stream(dev);
-    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, col, val, tile_aux,
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, flag_bits, col, val, tile_aux,
               nonempty_rows, carry, x_dev, y_dev, scale};
     std::vector<cudaEvent_t> evs;
     auto event_on = [&](cudaStream_t st) {
@@ -474,7 +516,8 @@ extern "C" int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz,
 }
 
 extern "C" int spmvb_spmv_csr5_tiles(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
-                                     const int32_t* tile_ptr, const uint8_t* bit_flag, const int32_t* col,
+                                     const int32_t* tile_ptr, const uint8_t* bit_flag, const uint32_t* flag_bits,
+                                     const int32_t* col,
                                      const double* val, const uint32_t* tile_aux, const int32_t* nonempty_rows,
                                      int64_t n_nonempty, double* carry, const double* x, double* y,
                                      const double* scale, int64_t t_begin, int64_t t_end, int64_t row_begin,
@@ -492,8 +535,17 @@ extern "C" int spmvb_spmv_csr5_tiles(int64_t n_rows, int64_t nnz, const int32_t*
         SPMVB_CUDA(cudaMemsetAsync(y + row_begin, 0, (row_end - row_begin) * sizeof(double), s));
       return;
     }
-    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, col, val, tile_aux,
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, flag_bits, col, val, tile_aux,
               nonempty_rows, carry, x, y, scale};
     launch_range(C, t_begin, t_end, row_begin, row_end, s);
+  });
+}
+
+extern "C" int spmvb_csr5_pack_flags(int64_t nnz, const uint8_t* bit_flag, uint32_t* flag_bits, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (nnz <= 0) return;
+    k_csr5_pack_flags<<<grid_for((nnz + 31) / 32 * 32, 256, 148 * 16), 256, 0, s>>>(nnz, bit_flag, flag_bits);
+    SPMVB_LAUNCHED("k_csr5_pack_flags");
   });
 }

@@ -162,6 +162,7 @@ class Csr5Matrix:
         self.tile_aux = tile_aux
         self.nonempty_rows = nonempty_rows
         self.n_nonempty = int(n_nonempty)
+        self.flag_bits = None  # bit_flag packed one bit per entry (set by to_csr5)
         self._ranges = {}
 
     @property
@@ -409,8 +410,13 @@ def to_csr5(a, omega: int, sigma: int) -> Csr5Matrix:
         if nnz and nonempty < csr.n_rows:
             rows = _i32(nonempty, dev)
             check(LIB.spmvb_csr_nonempty_rows(ptr(csr.ptr), csr.n_rows, ptr(rows), s))
-    return Csr5Matrix(csr.n_rows, csr.n_cols, csr.ptr, omega, sigma, num_tiles, tile_ptr, bit_flag, y_off, seg_off,
-                      col, val, aux, rows, nonempty)
+        # kernel-side: the flags packed one bit per entry (64 B per 512-entry tile)
+        bits = _i32((nnz + 31) // 32, dev)
+        check(LIB.spmvb_csr5_pack_flags(nnz, ptr(bit_flag), ptr(bits), s))
+    m = Csr5Matrix(csr.n_rows, csr.n_cols, csr.ptr, omega, sigma, num_tiles, tile_ptr, bit_flag, y_off, seg_off,
+                   col, val, aux, rows, nonempty)
+    m.flag_bits = bits
+    return m
 
 
 def to_ell(a, max_cells: int = DEFAULT_MAX_GRID_CELLS) -> EllMatrix:

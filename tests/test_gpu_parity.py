@@ -187,6 +187,31 @@ def test_host_buffers(sp, rng):
     assert sp.spmv("csr5", e, np.ones(4)).tolist() == [0.0] * 5
 
 
+def test_packed_flags_identical(sp, rng, monkeypatch):
+    """The tile kernel's packed-flag path (one bit per entry, used when x
+    exceeds L2) gives the same bits as the byte-flag path, for every
+    specialised (omega, sigma), on the device, streamed-host and range paths."""
+    from paper_1805_11938_b200 import kernels
+
+    r, c, v = sp.synth.rmat_triplets(scale=13, edge_factor=12, seed=11)
+    a = sp.canonicalize(r, c, v, 1 << 13, 1 << 13)
+    x = rng.uniform(-1.0, 1.0, size=1 << 13)
+    xd = torch.from_numpy(x).cuda()
+    for om, sg in [(32, 16), (16, 16), (8, 16), (4, 16), (32, 8), (16, 8), (8, 8), (4, 8)]:
+        m = sp.to_csr5(a, om, sg)
+        assert m.flag_bits is not None
+        monkeypatch.setattr(kernels, "_PACKED_FLAGS_MIN_X_BYTES", 1 << 62)
+        yb = np_(sp.spmv("csr5", m, xd))
+        monkeypatch.setattr(kernels, "_PACKED_FLAGS_MIN_X_BYTES", 0)
+        assert same_bits(sp.spmv("csr5", m, xd), yb), (om, sg)
+        assert same_bits(sp.spmv_csr5(m, x, ranges=5), yb), (om, sg)
+        bits = np_(m.flag_bits).view(np.uint32)
+        flags = np_(m.bit_flag).astype(np.uint32)
+        padded = np.zeros(bits.size * 32, dtype=np.uint32)
+        padded[: flags.size] = flags
+        assert np.array_equal(bits, (padded.reshape(-1, 32) << np.arange(32, dtype=np.uint32)).sum(1)), (om, sg)
+
+
 def test_errors(sp):
     r, c, v = demo_triplets()
     a = sp.canonicalize(r, c, v, 4, 4)
