@@ -261,12 +261,15 @@ int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* 
  * spmvb_sell_wide_plan and summed by a CTA each (within tolerance). */
 #define SPMVB_SELL_WIDE_COLS 256
 /* Also reports (host, may be NULL) the widest slice left to the per-row
- * kernel, which spmvb_spmv_sell uses to pick its slot loop (-1 = unknown). */
+ * kernel, which spmvb_spmv_sell uses to pick its slot loop (-1 = unknown),
+ * and (first_piece_out: device, n_slices entries; n_pieces: host) how the
+ * wide slices split into pieces of ~32K cells, one CTA each. */
 int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out, int64_t* n_wide,
-                         int64_t* max_narrow_width, void* stream);
+                         int64_t* max_narrow_width, int32_t* first_piece_out, int64_t* n_pieces, void* stream);
 int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                     const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
-                    int64_t max_narrow_width, const double* x, double* y, const double* scale, void* stream);
+                    const int32_t* first_piece, int64_t n_pieces, int64_t max_narrow_width, const double* x,
+                    double* y, const double* scale, void* stream);
 
 /* ||y||^2 over n entries into *out (device), deterministic two-level sum.
  * Used by power iteration. */

@@ -48,53 +48,114 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE == 2 ? 5 : 4)) k_sp
   }
 }
 
-// Wide slices (width > SPMVB_SELL_WIDE_COLS, power-law rows): one CTA per
-// slice, 256/rows threads per row each summing every (256/rows)-th column
-// (coalesced: consecutive threads read consecutive column-major cells), then
-// a fixed-order per-row sum of the thread partials (deterministic; not the
-// reference's sequential order, so within tolerance rather than bit-exact).
-__global__ void __launch_bounds__(256) k_spmv_sell_wide(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide,
+// Wide slices (width > SPMVB_SELL_WIDE_COLS, power-law rows; up to 128
+// rows): split into pieces of about SELL_PIECE_CELLS cells (whole columns),
+// one CTA per piece.  256/rows threads per row each sum every (256/rows)-th
+// column of the piece (coalesced: consecutive threads read consecutive
+// column-major cells), a fixed-order per-row sum of the thread partials goes
+// to the piece's slot, and a second kernel adds each row's pieces in order.
+// Deterministic; not the reference's sequential order, so within tolerance
+// rather than bit-exact.  (One CTA per whole slice serialised the widest
+// R-MAT slices: 33 ms of a C5 SELL SpMV.)
+constexpr int64_t SELL_PIECE_CELLS = 32768;
+constexpr int SELL_PART_STRIDE = 128;  // partial slots per piece (max rows of a wide slice)
+
+__device__ __forceinline__ int64_t sell_piece_cols(int rows_s) {
+  const int64_t pc = SELL_PIECE_CELLS / rows_s;
+  return pc < 256 ? 256 : pc;
+}
+
+__device__ __forceinline__ int sell_rows(int64_t sl, int64_t c, int64_t n_rows) {
+  return static_cast<int>((sl + 1) * c <= n_rows ? c : n_rows - sl * c);
+}
+
+// pieces per wide slice
+__global__ void k_sell_wide_pieces(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
+                                   const int64_t* __restrict__ widths, int32_t* __restrict__ pieces) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_wide;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t sl = wide[i];
+    const int64_t pc = sell_piece_cols(sell_rows(sl, c, n_rows));
+    pieces[i] = static_cast<int32_t>((widths[sl] + pc - 1) / pc);
+  }
+}
+
+// One CTA per piece (grid-stride over the device-side piece count).
+__global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide,
+                                                        int64_t n_wide, const int32_t* __restrict__ first_piece,
+                                                        int64_t n_pieces,
                                                         const int64_t* __restrict__ widths,
                                                         const int64_t* __restrict__ slice_off,
-                                                        const int32_t* __restrict__ perm,
                                                         const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                                        const double* __restrict__ x, double* __restrict__ y,
-                                                        const double* __restrict__ scale_p) {
+                                                        const double* __restrict__ x, double* __restrict__ part) {
   __shared__ double red[256];
   const int t = threadIdx.x;
-  const int64_t sl = wide[blockIdx.x];
-  const int rows_s = static_cast<int>((sl + 1) * c <= n_rows ? c : n_rows - sl * c);
-  const int nsub = 256 / rows_s;
-  const int sub = t / rows_s, l = t - sub * rows_s;
-  const int64_t w = widths[sl];
-  const int64_t base = slice_off[sl];
-  double acc = 0.0;
-  if (sub < nsub) {
-    int64_t j = sub;
-    for (; j + 3 * nsub < w; j += 4 * nsub) {
-      const int64_t o = base + j * rows_s + l, st = static_cast<int64_t>(nsub) * rows_s;
-      const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + st);
-      const double v2 = ld_stream(val + o + 2 * st), v3 = ld_stream(val + o + 3 * st);
-      const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + st);
-      const int32_t c2 = ld_stream(idx + o + 2 * st), c3 = ld_stream(idx + o + 3 * st);
-      acc += v0 * ldx(x, c0);
-      acc += v1 * ldx(x, c1);
-      acc += v2 * ldx(x, c2);
-      acc += v3 * ldx(x, c3);
+  for (int32_t item = blockIdx.x; item < n_pieces; item += gridDim.x) {
+    // wide slice holding this piece: last i with first_piece[i] <= item
+    int64_t lo = 0, hi = n_wide - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (first_piece[mid] <= item) lo = mid;
+      else hi = mid - 1;
     }
-    for (; j < w; j += nsub) {
-      const int64_t o = base + j * rows_s + l;
-      acc += ld_stream(val + o) * ldx(x, ld_stream(idx + o));
+    const int64_t sl = wide[lo];
+    const int rows_s = sell_rows(sl, c, n_rows);
+    const int64_t pc = sell_piece_cols(rows_s);
+    const int64_t j0 = static_cast<int64_t>(item - first_piece[lo]) * pc;
+    const int64_t w = widths[sl];
+    const int64_t j1 = j0 + pc < w ? j0 + pc : w;
+    const int nsub = 256 / rows_s;
+    const int sub = t / rows_s, l = t - sub * rows_s;
+    const int64_t base = slice_off[sl];
+    double acc = 0.0;
+    if (sub < nsub) {
+      const int64_t st = static_cast<int64_t>(nsub) * rows_s;
+      int64_t j = j0 + sub;
+      for (; j + 3 * nsub < j1; j += 4 * nsub) {
+        const int64_t o = base + j * rows_s + l;
+        const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + st);
+        const double v2 = ld_stream(val + o + 2 * st), v3 = ld_stream(val + o + 3 * st);
+        const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + st);
+        const int32_t c2 = ld_stream(idx + o + 2 * st), c3 = ld_stream(idx + o + 3 * st);
+        acc += v0 * ldx(x, c0);
+        acc += v1 * ldx(x, c1);
+        acc += v2 * ldx(x, c2);
+        acc += v3 * ldx(x, c3);
+      }
+      for (; j < j1; j += nsub) {
+        const int64_t o = base + j * rows_s + l;
+        acc += ld_stream(val + o) * ldx(x, ld_stream(idx + o));
+      }
     }
+    red[t] = acc;
+    __syncthreads();
+    if (t < rows_s) {
+      double sum = 0.0;
+      for (int k = 0; k < nsub; ++k) sum += red[t + k * rows_s];
+      part[static_cast<int64_t>(item) * SELL_PART_STRIDE + t] = sum;
+    }
+    __syncthreads();
   }
-  red[t] = acc;
-  __syncthreads();
-  if (t < rows_s) {
-    double s = 0.0;
-    for (int k = 0; k < nsub; ++k) s += red[t + k * rows_s];
-    const int64_t p = sl * c + t;
+}
+
+// Thread per (wide slice, row): the row's pieces in order.
+__global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
+                                  const int32_t* __restrict__ first_piece, int64_t n_pieces,
+                                  const double* __restrict__ part, const int32_t* __restrict__ perm,
+                                  double* __restrict__ y, const double* __restrict__ scale_p) {
+  const double sc = load_scale(scale_p);
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n_wide * c;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = q / c;
+    const int l = static_cast<int>(q - i * c);
+    const int64_t sl = wide[i];
+    if (l >= sell_rows(sl, c, n_rows)) continue;
+    const int32_t p0 = first_piece[i], p1 = i + 1 < n_wide ? first_piece[i + 1] : static_cast<int32_t>(n_pieces);
+    double sum = 0.0;
+    for (int32_t pc = p0; pc < p1; ++pc) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
+    const int64_t p = sl * c + l;
     const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
-    y[r] = scale_p ? load_scale(scale_p) * s : s;
+    y[r] = scale_p ? sc * sum : sum;
   }
 }
 
@@ -110,11 +171,13 @@ __global__ void k_sell_mark_wide(const int64_t* __restrict__ widths, int64_t n_r
 }  // namespace
 
 extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out,
-                                    int64_t* n_wide, int64_t* max_narrow_width, void* stream) {
+                                    int64_t* n_wide, int64_t* max_narrow_width, int32_t* first_piece_out,
+                                    int64_t* n_pieces, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     *n_wide = 0;
     if (max_narrow_width) *max_narrow_width = 0;
+    if (n_pieces) *n_pieces = 0;
     if (n_rows <= 0 || c < 1) return;
     const int64_t n_slices = (n_rows + c - 1) / c;
     DevBuf<uint8_t> flag(n_slices, s);
@@ -138,6 +201,17 @@ extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* wi
           mx.get(), s);
       copy_to_host(max_narrow_width, mx.get(), 1, s);
     }
+    if (h > 0 && first_piece_out && n_pieces) {
+      // pieces of ~SELL_PIECE_CELLS cells per wide slice, as a prefix
+      DevBuf<int32_t> np(h, s), tp(1, s);
+      k_sell_wide_pieces<<<grid_for(h, 256), 256, 0, s>>>(n_rows, c, wide_out, h, widths, np.get());
+      SPMVB_LAUNCHED("k_sell_wide_pieces");
+      exclusive_scan<int32_t>(h, ArrayLoad<int32_t>{np.get()}, ArrayStore<int32_t>{first_piece_out}, OpSum{}, 0,
+                              tp.get(), s);
+      int32_t hp = 0;
+      copy_to_host(&hp, tp.get(), 1, s);
+      *n_pieces = hp;
+    }
   });
 }
 
@@ -154,8 +228,9 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
 
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
-                               int64_t n_wide, int64_t max_narrow_width, const double* x, double* y,
-                               const double* scale, void* stream) {
+                               int64_t n_wide, const int32_t* first_piece, int64_t n_pieces,
+                               int64_t max_narrow_width, const double* x, double* y, const double* scale,
+                               void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
@@ -168,9 +243,14 @@ extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths,
     else k_spmv_sell<0><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_sell");
     if (n_wide > 0) {
-      k_spmv_sell_wide<<<static_cast<unsigned>(n_wide), 256, 0, s>>>(n_rows, c, wide, widths, slice_off, perm, idx,
-                                                                     val, x, y, scale);
-      SPMVB_LAUNCHED("k_spmv_sell_wide");
+      if (!first_piece || n_pieces < n_wide) fail(SPMVB_INVALID_ARG, "wide-slice piece plan missing");
+      DevBuf<double> part(static_cast<size_t>(n_pieces) * SELL_PART_STRIDE, s);
+      k_sell_wide_part<<<grid_for(n_pieces, 1, 148 * 16), 256, 0, s>>>(n_rows, c, wide, n_wide, first_piece, n_pieces,
+                                                                       widths, slice_off, idx, val, x, part.get());
+      SPMVB_LAUNCHED("k_sell_wide_part");
+      k_sell_wide_final<<<grid_for(n_wide * c, 256), 256, 0, s>>>(n_rows, c, wide, n_wide, first_piece, n_pieces,
+                                                                  part.get(), perm, y, scale);
+      SPMVB_LAUNCHED("k_sell_wide_final");
     }
   });
 }

@@ -276,17 +276,19 @@ class SellMatrix:
         self._wide = None
 
     def wide_plan(self):
-        """(wide slice list, count, widest remaining slice): slices wider than
-        SPMVB_SELL_WIDE_COLS get a CTA each (kernel-side, built once)."""
+        """(wide slice list, count, widest remaining slice, first piece per
+        wide slice, piece count): slices wider than SPMVB_SELL_WIDE_COLS are
+        cut into ~32K-cell pieces, a CTA each (kernel-side, built once)."""
         if self._wide is None:
             n_slices = self.n_slices
             lst = _i32(max(n_slices, 1), self.device)
-            cnt = ctypes.c_int64()
-            mx = ctypes.c_int64()
+            first = _i32(max(n_slices, 1), self.device)
+            cnt, mx, npieces = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
             with torch.cuda.device(self.device):
                 check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), ptr(lst), ctypes.byref(cnt),
-                                               ctypes.byref(mx), _lib.stream(self.device)))
-            self._wide = (lst, int(cnt.value), int(mx.value))
+                                               ctypes.byref(mx), ptr(first), ctypes.byref(npieces),
+                                               _lib.stream(self.device)))
+            self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value))
         return self._wide
 
     def _host_layout(self):

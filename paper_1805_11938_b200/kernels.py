@@ -235,14 +235,14 @@ def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
 def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
     """y = A x for SELL / SELL-C-sigma, scattered through perm (kernels.py:119-136)."""
 
-    wide, n_wide, max_narrow = m.wide_plan()
+    wide, n_wide, max_narrow, first_piece, n_pieces = m.wide_plan()
 
     def launch(xd, y, sp, s):
         perm = m.perm if m.sigma > 0 else None
         check(
             LIB.spmvb_spmv_sell(
                 m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
-                ptr(wide), n_wide, max_narrow, ptr(xd), ptr(y), sp, s,
+                ptr(wide), n_wide, ptr(first_piece), n_pieces, max_narrow, ptr(xd), ptr(y), sp, s,
             )
         )
 
