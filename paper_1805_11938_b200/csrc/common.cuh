@@ -131,6 +131,30 @@ inline int num_sms() {
   return sms;
 }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while its predecessor in the stream is still draining; it must call
+// pdl_wait() before touching anything the predecessor writes (or writing
+// anything the predecessor reads).  In a kernel launched normally the wait
+// returns at once.  Chained SpMV -> fix-up -> norm -> scale kernels thereby
+// overlap each launch with the previous kernel's tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SPMVB_CUDA(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 inline unsigned grid_for(int64_t n, int block, int64_t cap = (1ll << 30)) {
   int64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;

@@ -134,6 +134,7 @@ __global__ void k_spmv_sequential(int64_t n_rows, const int32_t* __restrict__ pt
 }
 
 __global__ void k_inv_sqrt(const double* sumsq, double* scale) {
+  pdl_wait();
   double s = *sumsq;
   *scale = (s > 0.0) ? 1.0 / sqrt(s) : 1.0;
 }
@@ -369,14 +370,14 @@ extern "C" int spmvb_sumsq(const double* y, int64_t n, double* out, void* stream
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     device_reduce<double>(
-        n, [=] __device__(int64_t i) { double v = y[i]; return v * v; }, OpSum{}, 0.0, out, s);
+        n, [=] __device__(int64_t i) { double v = y[i]; return v * v; }, OpSum{}, 0.0, out, s, /*pdl=*/true);
   });
 }
 
 extern "C" int spmvb_inv_sqrt(const double* sumsq, double* scale_out, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
-    k_inv_sqrt<<<1, 1, 0, s>>>(sumsq, scale_out);
+    launch_pdl(k_inv_sqrt, dim3(1), dim3(1), 0, s, sumsq, scale_out);
     SPMVB_LAUNCHED("k_inv_sqrt");
   });
 }

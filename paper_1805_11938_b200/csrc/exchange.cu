@@ -106,7 +106,7 @@ __global__ void k_sum_inv_sqrt(const double* __restrict__ vals, int n, double* _
   double s = 0.0;
   for (int i = 0; i < n; ++i) s += vals[i];
   *sumsq = s;
-  *scale = 1.0 / sqrt(s);
+  *scale = (s > 0.0) ? 1.0 / sqrt(s) : 1.0;  // as spmvb_inv_sqrt
 }
 
 }  // namespace

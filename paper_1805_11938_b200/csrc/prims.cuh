@@ -89,6 +89,7 @@ constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 template <typename T, typename Load, typename Op>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_tile_reduce(int64_t n, Load load, Op op, T identity,
                                                                    T* tile_out) {
+  pdl_wait();
   __shared__ T tmp[SCAN_THREADS / 32 + 1];
   int64_t base = static_cast<int64_t>(blockIdx.x) * SCAN_TILE;
   T acc = identity;
@@ -176,6 +177,7 @@ void exclusive_scan(int64_t n, Load load, Store store, Op op, T identity, T* tot
 // Device-wide reduction to a device scalar.
 template <typename T, typename Load, typename Op>
 __global__ void __launch_bounds__(SCAN_THREADS) k_reduce_final(int64_t n, Load load, Op op, T identity, T* out) {
+  pdl_wait();
   __shared__ T tmp[SCAN_THREADS / 32 + 1];
   T acc = identity;
   for (int64_t i = threadIdx.x; i < n; i += SCAN_THREADS) acc = op(acc, load(i));
@@ -183,18 +185,25 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_reduce_final(int64_t n, Load l
   if (threadIdx.x == 0) *out = r;
 }
 
+// pdl: launch as programmatic dependents of the preceding kernel (see
+// launch_pdl); the kernels wait for it before reading.
 template <typename T, typename Load, typename Op>
-void device_reduce(int64_t n, Load load, Op op, T identity, T* out, cudaStream_t s) {
+void device_reduce(int64_t n, Load load, Op op, T identity, T* out, cudaStream_t s, bool pdl = false) {
   if (n <= SCAN_TILE) {
-    k_reduce_final<T><<<1, SCAN_THREADS, 0, s>>>(n, load, op, identity, out);
+    if (pdl) launch_pdl(k_reduce_final<T, Load, Op>, dim3(1), dim3(SCAN_THREADS), 0, s, n, load, op, identity, out);
+    else k_reduce_final<T><<<1, SCAN_THREADS, 0, s>>>(n, load, op, identity, out);
     SPMVB_LAUNCHED("k_reduce_final");
     return;
   }
   int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   DevBuf<T> part(tiles, s);
-  k_scan_tile_reduce<T><<<static_cast<unsigned>(tiles), SCAN_THREADS, 0, s>>>(n, load, op, identity, part.get());
+  if (pdl)
+    launch_pdl(k_scan_tile_reduce<T, Load, Op>, dim3(static_cast<unsigned>(tiles)), dim3(SCAN_THREADS), 0, s, n,
+               load, op, identity, part.get());
+  else
+    k_scan_tile_reduce<T><<<static_cast<unsigned>(tiles), SCAN_THREADS, 0, s>>>(n, load, op, identity, part.get());
   SPMVB_LAUNCHED("k_scan_tile_reduce");
-  device_reduce<T>(tiles, ArrayLoad<T>{part.get()}, op, identity, out, s);
+  device_reduce<T>(tiles, ArrayLoad<T>{part.get()}, op, identity, out, s, pdl);
 }
 
 // ---------------------------------------------------------------------------

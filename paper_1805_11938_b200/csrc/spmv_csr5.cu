@@ -152,19 +152,20 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
 template <int W, int S>
 __global__ void __launch_bounds__(256, 4) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
                                                      int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
-  if (rows_per_block > 0) {
-    const int64_t r0 = row_begin + blockIdx.x * rows_per_block;
-    const int64_t r1 = r0 + rows_per_block < row_end ? r0 + rows_per_block : row_end;
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
-      if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
-  }
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
   const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
+  auto zero_empty_rows = [&] {  // this block's slice of the empty rows
+    if (rows_per_block > 0) {
+      const int64_t r0 = row_begin + blockIdx.x * rows_per_block;
+      const int64_t r1 = r0 + rows_per_block < row_end ? r0 + rows_per_block : row_end;
+      for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+        if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
+    }
+  };
   const bool active = group < t_end;
   const int64_t t = active ? group : t_begin;
   const int64_t tile0 = t * static_cast<int64_t>(W) * S;
-  const double sc = load_scale(C.scale_p);
   uint32_t fmask = 0;
   int32_t cidx[S];
   double v[S];
@@ -202,9 +203,17 @@ __global__ void __launch_bounds__(256, 4) k_csr5_warp_s(Csr5Ctx C, int64_t t_beg
         v[i] = ld_stream(C.val + base + i * W);
       }
     }
+    // the matrix loads above may overlap the previous kernel's tail (PDL);
+    // x, scale and y only after it has finished
+    pdl_wait();
+    zero_empty_rows();
 #pragma unroll
     for (int i = 0; i < S; ++i) v[i] *= ldx(C.x, cidx[i]);
-  } else if (active) {
+  } else {
+    pdl_wait();
+    zero_empty_rows();
+  }
+  if (active && tile0 + W * S > C.nnz) {
     // partial tile: every load is issued (clamped to the tile start when the
     // cell is unoccupied) before any is used
     const int64_t m = C.nnz - tile0;
@@ -227,6 +236,7 @@ __global__ void __launch_bounds__(256, 4) k_csr5_warp_s(Csr5Ctx C, int64_t t_beg
       v[i] = ok ? v[i] * ldx(C.x, cidx[i]) : 0.0;
     }
   }
+  const double sc = load_scale(C.scale_p);
   const uint32_t aux = active ? C.aux[t] : 0u;
   const int nflags = __popc(fmask);
   int incl = nflags;
@@ -274,6 +284,7 @@ __global__ void __launch_bounds__(256, 4) k_csr5_warp_s(Csr5Ctx C, int64_t t_beg
 __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __restrict__ tile_ptr,
                              const uint32_t* __restrict__ aux, const double* __restrict__ carry,
                              double* __restrict__ y) {
+  pdl_wait();  // launched as a programmatic dependent of the tile kernel
   // chain key = the continued row, tile_ptr[t] (coalesced, loaded alongside
   // aux[t] rather than after it)
   fold_chains(
@@ -319,7 +330,8 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
   auto warp_s_launch = [&](auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
     const int64_t blocks = ((t_end - t_begin) * W + 255) / 256;
     const int64_t rpb = empties ? (row_end - row_begin + blocks - 1) / blocks : 0;
-    kern<<<static_cast<unsigned>(blocks), 256, 0, s>>>(C, t_begin, t_end, rpb, row_begin, row_end);
+    launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, C, t_begin, t_end, rpb, row_begin,
+               row_end);
     SPMVB_LAUNCHED("k_csr5_warp_s");
     generic_begin = t_end;
   };
@@ -357,7 +369,8 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
   }
   if (t_end - t_begin > 1 || t_begin > 0) {
     // one 32-tile window per warp: every window's loads are in flight at once
-    k_csr5_fixup<<<grid_for(t_end - t_begin, 256), 256, 0, s>>>(t_begin, t_end, C.tile_ptr, C.aux, C.carry, C.y);
+    launch_pdl(k_csr5_fixup, dim3(grid_for(t_end - t_begin, 256)), dim3(256), 0, s, t_begin, t_end, C.tile_ptr,
+               C.aux, C.carry, C.y);
     SPMVB_LAUNCHED("k_csr5_fixup");
   }
 }
