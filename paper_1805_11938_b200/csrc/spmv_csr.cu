@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     const double* __restrict__ ell_val, int64_t rows_per_block) {
   static_assert(S == 8, "lane-contiguous loads assume 8 entries (32 B of indices) per lane");
   constexpr int CH = 32 * S;
+  pdl_wait();
   if (rows_per_block > 0) {
     // this block's slice of the empty rows (HYB: rows whose tail is empty get
     // their ELL part), riding along with the gather-bound chunk work
@@ -194,6 +195,7 @@ __global__ void k_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, in
 // the same) into its row, chain by chain in chunk order (fold_chains).
 __global__ void k_chunk_fixup(int64_t num, const int32_t* __restrict__ carry_row, const double* __restrict__ carry_val,
                               double* __restrict__ y, const double* __restrict__ scale_p) {
+  pdl_wait();
   const double sc = load_scale(scale_p);
   fold_chains(
       0, num, [&](int64_t c) { return carry_row[c]; }, [&](int64_t c) { return carry_val[c]; },
@@ -224,9 +226,9 @@ void launch_main(const ChunkArgs& a, int64_t nchunks, bool empties, cudaStream_t
   const size_t smem = sizeof(ChunkSmem<S>);
   const int64_t blocks = (nchunks + CK_WARPS - 1) / CK_WARPS;
   const int64_t rpb = empties ? (a.n_rows + blocks - 1) / blocks : 0;
-  k_spmv_chunk<S, HAS_ELL, VEC><<<static_cast<unsigned>(blocks), CK_WARPS * 32, smem, s>>>(
-      a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x, a.y,
-      a.scale, a.ell_k, a.ell_idx, a.ell_val, rpb);
+  launch_pdl(k_spmv_chunk<S, HAS_ELL, VEC>, dim3(static_cast<unsigned>(blocks)), dim3(CK_WARPS * 32), smem, s,
+             a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x,
+             a.y, a.scale, a.ell_k, a.ell_idx, a.ell_val, rpb);
   SPMVB_LAUNCHED("k_spmv_chunk");
 }
 
@@ -247,7 +249,8 @@ void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
   if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, empties, s);
   else launch_main<S, HAS_ELL, false>(a, nchunks, empties, s);
   if (nchunks > 1) {
-    k_chunk_fixup<<<grid_for(nchunks, 256), 256, 0, s>>>(nchunks, a.carry_row, a.carry_val, a.y, a.scale);
+    launch_pdl(k_chunk_fixup, dim3(grid_for(nchunks, 256)), dim3(256), 0, s, nchunks, a.carry_row, a.carry_val, a.y,
+               a.scale);
     SPMVB_LAUNCHED("k_chunk_fixup");
   }
 }

@@ -15,6 +15,7 @@ namespace {
 template <bool PF>
 __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict__ idx, const double* __restrict__ val,
                            const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
+  pdl_wait();
   const double s = load_scale(scale_p);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -31,6 +32,7 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE == 2 ? 5 : 4)) k_sp
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
+  pdl_wait();
   const double s = load_scale(scale_p);
   const int32_t c32 = static_cast<int32_t>(c);  // n_rows < 2^31: 32-bit slice arithmetic
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n_rows;
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
                                                         const int64_t* __restrict__ slice_off,
                                                         const int32_t* __restrict__ idx, const double* __restrict__ val,
                                                         const double* __restrict__ x, double* __restrict__ part) {
+  pdl_wait();
   __shared__ double red[256];
   const int t = threadIdx.x;
   for (int32_t item = blockIdx.x; item < n_pieces; item += gridDim.x) {
@@ -143,6 +146,7 @@ __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __re
                                   const int32_t* __restrict__ first_piece, int64_t n_pieces,
                                   const double* __restrict__ part, const int32_t* __restrict__ perm,
                                   double* __restrict__ y, const double* __restrict__ scale_p) {
+  pdl_wait();
   const double sc = load_scale(scale_p);
   for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n_wide * c;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -220,8 +224,9 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
-    if (k > 8) k_spmv_ell<true><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, k, idx, val, x, y, scale);
-    else k_spmv_ell<false><<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, k, idx, val, x, y, scale);
+    const dim3 g(grid_for(n_rows, 256)), b(256);
+    if (k > 8) launch_pdl(k_spmv_ell<true>, g, b, 0, s, n_rows, k, idx, val, x, y, scale);
+    else launch_pdl(k_spmv_ell<false>, g, b, 0, s, n_rows, k, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_ell");
   });
 }
@@ -237,19 +242,18 @@ extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths,
     // c < 8: slot loads through L1 (the other half of each index sector is
     // the next slot's); wide rows (> 8 slots): next four slots prefetched
     const unsigned g = grid_for(n_rows, 256);
-    if (c < 8) k_spmv_sell<1><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
-    else if (max_narrow_width > 8 || max_narrow_width < 0)
-      k_spmv_sell<2><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
-    else k_spmv_sell<0><<<g, 256, 0, s>>>(n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
+    auto kern = c < 8 ? k_spmv_sell<1> : (max_narrow_width > 8 || max_narrow_width < 0) ? k_spmv_sell<2>
+                                                                                        : k_spmv_sell<0>;
+    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_sell");
     if (n_wide > 0) {
       if (!first_piece || n_pieces < n_wide) fail(SPMVB_INVALID_ARG, "wide-slice piece plan missing");
       DevBuf<double> part(static_cast<size_t>(n_pieces) * SELL_PART_STRIDE, s);
-      k_sell_wide_part<<<grid_for(n_pieces, 1, 148 * 16), 256, 0, s>>>(n_rows, c, wide, n_wide, first_piece, n_pieces,
-                                                                       widths, slice_off, idx, val, x, part.get());
+      launch_pdl(k_sell_wide_part, dim3(grid_for(n_pieces, 1, 148 * 16)), dim3(256), 0, s, n_rows, c, wide, n_wide,
+                 first_piece, n_pieces, widths, slice_off, idx, val, x, part.get());
       SPMVB_LAUNCHED("k_sell_wide_part");
-      k_sell_wide_final<<<grid_for(n_wide * c, 256), 256, 0, s>>>(n_rows, c, wide, n_wide, first_piece, n_pieces,
-                                                                  part.get(), perm, y, scale);
+      launch_pdl(k_sell_wide_final, dim3(grid_for(n_wide * c, 256)), dim3(256), 0, s, n_rows, c, wide, n_wide,
+                 first_piece, n_pieces, part.get(), perm, y, scale);
       SPMVB_LAUNCHED("k_sell_wide_final");
     }
   });
