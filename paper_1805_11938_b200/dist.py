@@ -371,6 +371,41 @@ class PowerIteration:
             self._allgatherv(self.x)
         return self.x
 
+    def run(self, steps: int, graph: bool = False) -> None:
+        """``steps`` power-iteration steps.  ``graph=True`` (single process)
+        captures two steps -- one x/x_next ping-pong -- in a CUDA graph once
+        and replays it, so launch-bound small matrices are not limited by
+        host-side launch cost; an odd remainder step runs eagerly."""
+        if not graph or self.world > 1 or self.device.type != "cuda":
+            for _ in range(steps):
+                self.step()
+            return
+        if getattr(self, "_graph", None) is None:
+            if steps < 2:
+                for _ in range(steps):
+                    self.step()
+                return
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):  # two real steps warm the allocations
+                self.step()
+                self.step()
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            steps -= 2
+            g = torch.cuda.CUDAGraph()
+            self._graph_x = self.x.data_ptr()  # the graph reads this buffer as x
+            with torch.cuda.graph(g):
+                self.step()
+                self.step()
+            self._graph = g
+        if steps and self.x.data_ptr() != self._graph_x:  # odd step count so far
+            self.step()
+            steps -= 1
+        for _ in range(steps // 2):
+            self._graph.replay()
+        if steps % 2:
+            self.step()
+
     def eigenvalue_estimate(self) -> float:
         """||A x_k|| for the current normalised iterate (1/scale)."""
         s = float(self.scale.item())
