@@ -314,12 +314,15 @@ def run_ours(args):
         pi.step()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
-    ramp_end = time.perf_counter() + args.clock_ramp_s
-    ramp_steps = 0
-    while time.perf_counter() < ramp_end:  # keep the GPU busy so clocks are sampled under load
+    # keep the GPU busy ~clock_ramp_s so clocks are sampled under load; the
+    # step count is fixed up front and agreed by all ranks (every step holds
+    # collectives, so ranks must run exactly the same number)
+    n_ramp = torch.tensor([int(args.clock_ramp_s / max(t_kernel, 1e-6))], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(n_ramp, op=dist.ReduceOp.MAX)
+    for i in range(int(n_ramp.item())):
         pi.step()
-        ramp_steps += 1
-        if ramp_steps % 50 == 0:
+        if i % 50 == 49:
             torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
