@@ -55,10 +55,17 @@ from .harness import (  # noqa: E402
     BenchConfig,
     BenchRecord,
     bandwidth_estimate,
+    bench_corpus,
     best_labels,
+    discover_corpus,
+    read_records,
+    record_from_line,
+    record_to_line,
     run_bench,
     spmv_bytes,
     spmv_flops,
+    times_by_matrix,
+    write_records,
 )
 from .kernels import spmv, spmv_csr, spmv_csr5, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
 from .model import DecisionTreeModel, ModelIOError, load_model, predict, select_format  # noqa: E402
