@@ -68,6 +68,13 @@ from .harness import (  # noqa: E402
     write_records,
 )
 from .kernels import spmv, spmv_csr, spmv_csr5, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
-from .model import DecisionTreeModel, ModelIOError, load_model, predict, select_format  # noqa: E402
+from .model import (  # noqa: E402
+    DecisionTreeModel,
+    ModelIOError,
+    load_model,
+    predict,
+    select_format,
+    select_format_measured,
+)
 
 __version__ = "0.1.0"

@@ -156,3 +156,52 @@ def load_model(source) -> DecisionTreeModel:
         if not node.is_leaf and not 0 <= node.feature < N_FEATURES:
             raise ModelIOError(f"split on unknown feature {node.feature}")
     return DecisionTreeModel(_ordered_tree(nodes), max_depth, min_leaf, ScalingParams(mins, maxs))
+
+
+# GPU-tuned conversion parameters of the measured selector (the bench's
+# candidates): wide CSR5 tiles and SELL slices.
+MEASURED_CANDIDATES = {
+    FormatTag.CSR: {},
+    FormatTag.CSR5: dict(omega=32, sigma=16),
+    FormatTag.ELL: {},
+    FormatTag.SELL: dict(sell_c=32, sell_sigma=1024),
+    FormatTag.HYB: {},
+}
+
+
+def select_format_measured(a, formats=None, *, params=None, reps: int = 10, warmup: int = 3):
+    """Measured-time selector (what the multi-GPU driver
+    does per shard): convert to each candidate format on the GPU, time its
+    SpMV with CUDA events on an all-ones x, keep the fastest.  Formats whose
+    conversion fails (ConversionError, out of memory) are skipped.  Returns
+    (tag, converted matrix, {tag: seconds per SpMV}); ties go to FormatTag
+    declaration order."""
+    import torch
+
+    from ._lib import ConversionError
+    from .kernels import spmv
+
+    tags = [FormatTag(f) for f in formats] if formats else list(FormatTag)
+    params = params or MEASURED_CANDIDATES
+    x = torch.ones(a.n_cols, dtype=torch.float64, device=a.row.device)
+    y = torch.empty(a.n_rows, dtype=torch.float64, device=a.row.device)
+    times, best = {}, None
+    for tag in tags:
+        try:
+            m = convert(tag, a, **params.get(tag, {}))
+        except (ConversionError, MemoryError):
+            continue
+        for _ in range(warmup):
+            spmv(tag, m, x, out=y)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            spmv(tag, m, x, out=y)
+        e1.record()
+        e1.synchronize()
+        times[tag] = e0.elapsed_time(e1) / 1e3 / reps
+        if best is None or times[tag] < times[best[0]]:
+            best = (tag, m)
+    if best is None:
+        raise ConversionError("no candidate format converted")
+    return best[0], best[1], times

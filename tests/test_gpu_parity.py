@@ -212,6 +212,21 @@ def test_packed_flags_identical(sp, rng, monkeypatch):
         assert np.array_equal(bits, (padded.reshape(-1, 32) << np.arange(32, dtype=np.uint32)).sum(1)), (om, sg)
 
 
+def test_select_format_measured(sp, rng):
+    """The measured selector returns the fastest converted format and its
+    matrix; ELL that cannot convert is skipped."""
+    r, c, v = sp.synth.rmat_triplets(scale=12, edge_factor=8, seed=2)
+    a = sp.canonicalize(r, c, v, 1 << 12, 1 << 12)
+    tag, m, times = sp.select_format_measured(a, reps=3,
+                                              params={sp.FormatTag.ELL: dict(max_cells=10)})
+    assert sp.FormatTag.ELL not in times and tag in times
+    assert times[tag] == min(times.values())
+    x = torch.from_numpy(rng.uniform(-1, 1, size=1 << 12)).cuda()
+    assert_within(sp.spmv(tag, m, x), sp.dense_spmv_oracle(a, x).cpu().numpy(),
+                  sp.dense_spmv_oracle(sp.canonicalize(np_(a.row), np_(a.col), np.abs(np_(a.data)), 1 << 12,
+                                                       1 << 12), torch.abs(x)).cpu().numpy())
+
+
 def test_errors(sp):
     r, c, v = demo_triplets()
     a = sp.canonicalize(r, c, v, 4, 4)
