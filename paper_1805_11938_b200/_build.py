@@ -32,6 +32,8 @@ NVCC_FLAGS = [
     "-Xcompiler",
     "-fPIC,-O2",
     f"-I{INCLUDE}",
+    # experiments only (e.g. -DSPMVB_CSR5_MINB=5); rebuild with force=True
+    *os.environ.get("SPMVB_NVCC_EXTRA", "").split(),
 ]
 
 

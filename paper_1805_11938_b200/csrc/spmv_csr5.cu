@@ -6,6 +6,10 @@
 
 #include "spmv_common.cuh"
 
+#ifndef SPMVB_CSR5_MINB
+#define SPMVB_CSR5_MINB 4  // resident blocks per SM the tile kernel is compiled for (64 registers)
+#endif
+
 using namespace spmvb;
 
 namespace {
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
 // block), so that streaming pass rides along with the gather-bound tiles
 // instead of costing its own launch.
 template <int W, int S>
-__global__ void __launch_bounds__(256, 4) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
+__global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
                                                      int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
