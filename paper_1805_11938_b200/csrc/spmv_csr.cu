@@ -79,8 +79,7 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     const int64_t r0 = blockIdx.x * rows_per_block;
     const int64_t r1 = r0 + rows_per_block < n_rows ? r0 + rows_per_block : n_rows;
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
-      if (ld_stream(ptr + r) == ld_stream(ptr + r + 1))
-        y[r] = HAS_ELL ? sc * ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x) : 0.0;
+      if (ld_stream(ptr + r) == ld_stream(ptr + r + 1)) y[r] = 0.0;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkSmem<S>& sm = *reinterpret_cast<ChunkSmem<S>*>(smem_raw);
@@ -130,9 +129,6 @@ __global__ void __launch_bounds__(CK_WARPS * 32) k_spmv_chunk(
     const int p = static_cast<int>((i == i0 ? p0 : ptr[r]) - k0);
     seg[p] = r;
     atomicOr(&flag[p >> 5], 1u << (p & 31));
-    // HYB: the row's ELL part, parked unscaled in y[r] for the lane that
-    // closes the row's segment
-    if (HAS_ELL) y[r] = ell_row<HAS_ELL>(n_rows, r, ell_k, ell_idx, ell_val, x);
   }
   __syncwarp();  // also orders the parked y[r] stores before the reads below
   // 3. lane-contiguous segments
@@ -221,11 +217,29 @@ struct ChunkArgs {
   const double* ell_val;
 };
 
+// HYB ELL part for every row, one coalesced thread-per-row pass: rows whose
+// tail is empty get their final value sc * ell; rows with a tail get ell
+// unscaled, parked in y for the chunk kernel, whose closing lane writes
+// sc * (ell + tail sum) -- the order the per-row fused version used.
+template <bool PF>
+__global__ void k_hyb_ell_prepass(int64_t n_rows, const int32_t* __restrict__ tail_ptr, int64_t k,
+                                  const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                  const double* __restrict__ x, double* __restrict__ y,
+                                  const double* __restrict__ scale_p) {
+  pdl_wait();
+  const double sc = load_scale(scale_p);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double e = PF ? seq_slots(k, n_rows, r, idx, val, x) : seq_slots4(k, n_rows, r, idx, val, x);
+    y[r] = ld_stream(tail_ptr + r) == ld_stream(tail_ptr + r + 1) ? sc * e : e;
+  }
+}
+
 template <int S, bool HAS_ELL, bool VEC>
 void launch_main(const ChunkArgs& a, int64_t nchunks, bool empties, cudaStream_t s) {
   const size_t smem = sizeof(ChunkSmem<S>);
   const int64_t blocks = (nchunks + CK_WARPS - 1) / CK_WARPS;
-  const int64_t rpb = empties ? (a.n_rows + blocks - 1) / blocks : 0;
+  const int64_t rpb = (empties && !HAS_ELL) ? (a.n_rows + blocks - 1) / blocks : 0;
   launch_pdl(k_spmv_chunk<S, HAS_ELL, VEC>, dim3(static_cast<unsigned>(blocks)), dim3(CK_WARPS * 32), smem, s,
              a.n_rows, a.nnz, a.ptr, a.col, a.val, a.nz_rows, a.chunk_row, nchunks, a.carry_row, a.carry_val, a.x,
              a.y, a.scale, a.ell_k, a.ell_idx, a.ell_val, rpb);
@@ -244,6 +258,16 @@ void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
       SPMVB_LAUNCHED("k_empty_rows");
     }
     return;
+  }
+  if (HAS_ELL) {
+    const dim3 g(grid_for(a.n_rows, 256)), b(256);
+    if (a.ell_k > 8)
+      launch_pdl(k_hyb_ell_prepass<true>, g, b, 0, s, a.n_rows, a.ptr, a.ell_k, a.ell_idx, a.ell_val, a.x, a.y,
+                 a.scale);
+    else
+      launch_pdl(k_hyb_ell_prepass<false>, g, b, 0, s, a.n_rows, a.ptr, a.ell_k, a.ell_idx, a.ell_val, a.x, a.y,
+                 a.scale);
+    SPMVB_LAUNCHED("k_hyb_ell_prepass");
   }
   // 256-bit loads need 32-byte aligned index/value arrays (torch allocations are)
   if (aligned32(a.col) && aligned32(a.val)) launch_main<S, HAS_ELL, true>(a, nchunks, empties, s);
