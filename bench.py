@@ -202,7 +202,8 @@ def run_ours(args):
     t_csr = time.perf_counter() - t0
     nnz = csr_full.nnz
     del a
-    bounds = spdist.nnz_balanced_bounds(csr_full.ptr, world)
+    bounds = (spdist.cost_balanced_bounds(csr_full.ptr, world) if args.balance == "cost"
+              else spdist.nnz_balanced_bounds(csr_full.ptr, world))
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     shard = spdist.row_block(csr_full, lo, hi) if world > 1 else csr_full
     if world > 1:
@@ -419,6 +420,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "format": tag, "params": formats[tag]["params"], "n": n,
                        "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
+                       "balance": args.balance,
                        "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"
                                 if world > 1 else "y=s*A x; ||y||^2; s=1/||y||"),
                        "l2": "inputs larger than L2 (matrix >= 6 GB), no flush"},
@@ -456,6 +458,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--overlap-ranges", type=int, default=4,
                     help="N > 1, CSR5 shards: row ranges whose all-gatherv overlaps the remaining local SpMV")
+    ap.add_argument("--balance", choices=["nnz", "cost"], default="nnz",
+                    help="N > 1 row blocks: nnz-balanced (the config's) or nnz + 1.5 rows (see dist.cost_balanced_bounds)")
     ap.add_argument("--compare-p2p", action="store_true",
                     help="N > 1: also time the peer-memory exchange (symmetric memory) next to the default")
     ap.add_argument("--exchange", choices=["allgatherv", "sparse", "p2p"], default="allgatherv",

@@ -47,7 +47,7 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import CsrMatrix
 
-__all__ = ["nnz_balanced_bounds", "row_block", "PowerIteration", "GpuOps"]
+__all__ = ["nnz_balanced_bounds", "cost_balanced_bounds", "row_block", "PowerIteration", "GpuOps"]
 
 
 def nnz_balanced_bounds(row_ptr, parts: int) -> np.ndarray:
@@ -58,6 +58,24 @@ def nnz_balanced_bounds(row_ptr, parts: int) -> np.ndarray:
     nnz = int(p_host[-1])
     targets = [-(-p * nnz // parts) for p in range(1, parts)]
     inner = np.searchsorted(p_host, targets, side="left") if parts > 1 else np.empty(0, np.int64)
+    bounds = np.concatenate([[0], np.minimum(inner, n), [n]]).astype(np.int64)
+    return np.maximum.accumulate(bounds)
+
+
+def cost_balanced_bounds(row_ptr, parts: int, row_weight: float = 1.5) -> np.ndarray:
+    """Row blocks balanced on nnz + row_weight * rows instead of nnz alone.
+
+    A shard's SpMV time is not only its nonzeros: every row costs a y store
+    (and the empty-row pass a ptr test), so on R-MAT the nnz-balanced shard
+    holding the long tail of light rows is the slowest (C5, P = 8: 0.43 vs
+    0.32 ms, profiles/r01_c5_shards.jsonl; fitting those shard times gives
+    one row ~ 1.5 nonzeros).  r_p = first row whose prefix cost reaches
+    p/P of the total."""
+    p_host = row_ptr.cpu().numpy() if isinstance(row_ptr, torch.Tensor) else np.asarray(row_ptr)
+    n = p_host.size - 1
+    cost = p_host.astype(np.float64) + row_weight * np.arange(n + 1, dtype=np.float64)
+    targets = [p * cost[-1] / parts for p in range(1, parts)]
+    inner = np.searchsorted(cost, targets, side="left") if parts > 1 else np.empty(0, np.int64)
     bounds = np.concatenate([[0], np.minimum(inner, n), [n]]).astype(np.int64)
     return np.maximum.accumulate(bounds)
 

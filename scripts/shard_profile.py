@@ -39,14 +39,16 @@ def main():
     csr = sp.to_csr(a)
     del a
     x = synth.uniform_vector(n, 7, device=dev)
+    balance = sys.argv[3] if len(sys.argv) > 3 else "nnz"
     for P in (1, 2, 4, 8):
-        bounds = spdist.nnz_balanced_bounds(csr.ptr, P)
+        bounds = (spdist.cost_balanced_bounds(csr.ptr, P) if balance == "cost"
+                  else spdist.nnz_balanced_bounds(csr.ptr, P))
         for p in range(P):
             lo, hi = int(bounds[p]), int(bounds[p + 1])
             shard = spdist.row_block(csr, lo, hi) if P > 1 else csr
-            rec = {"P": P, "shard": p, "rows": hi - lo, "nnz": shard.nnz}
+            rec = {"P": P, "shard": p, "balance": balance, "rows": hi - lo, "nnz": shard.nnz}
             best = None
-            for tag, kw in (("csr5", dict(omega=32, sigma=16)), ("csr", {})):
+            for tag, kw in (("csr5", dict(omega=32, sigma=16)),):
                 m = sp.convert(tag, shard, **kw)
                 y = torch.empty(m.n_rows, dtype=torch.float64, device=dev)
                 ms = event_ms(lambda: sp.spmv(tag, m, x, out=y))

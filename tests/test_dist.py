@@ -132,6 +132,20 @@ def test_partition_is_nnz_balanced_and_covers_rows():
             assert b[p] == 0 or ptr[b[p] - 1] < -(-p * nnz // parts)
 
 
+def test_cost_balanced_bounds():
+    from paper_1805_11938_b200 import dist as spdist
+
+    (ptr, ind, dat), n = _matrix()
+    for parts in (1, 2, 3, 8):
+        for w in (0.0, 1.5, 10.0):
+            b = spdist.cost_balanced_bounds(ptr, parts, row_weight=w)
+            assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0) and len(b) == parts + 1
+            cost = ptr + w * np.arange(n + 1)
+            for p in range(1, parts):
+                assert cost[b[p]] >= p * cost[-1] / parts
+                assert b[p] == 0 or cost[b[p] - 1] < p * cost[-1] / parts
+
+
 def test_two_rank_power_iteration_matches_serial():
     world, steps = 2, 12
     mgr = mp.Manager()
