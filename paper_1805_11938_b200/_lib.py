@@ -8,12 +8,14 @@ entry point without a CUDA device raises ``RuntimeError``.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().with_name("libspmvb.so")
+# SPMVB_LIB_PATH: another build of the same ABI (A/B experiments between builds only)
+_LIB_PATH = Path(os.environ.get("SPMVB_LIB_PATH") or Path(__file__).resolve().with_name("libspmvb.so"))
 
 SPMVB_OK = 0
 SPMVB_INVALID_ARG = 1

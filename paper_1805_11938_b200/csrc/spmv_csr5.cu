@@ -153,17 +153,47 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
 // of the empty rows of [row_begin, row_end) (a coalesced slice of ptr/y per
 // block), so that streaming pass rides along with the gather-bound tiles
 // instead of costing its own launch.
-template <int W, int S>
+template <int W, int S, bool EMPTIES>
 __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
                                                      int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
   const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
-  auto zero_empty_rows = [&] {  // this block's slice of the empty rows
+  const int64_t zr0 = EMPTIES ? row_begin + blockIdx.x * rows_per_block : 0;
+  const int64_t zr1 = EMPTIES ? (zr0 + rows_per_block < row_end ? zr0 + rows_per_block : row_end) : 0;
+  // This block's slice of the empty rows: the ptr pairs of its first ZP
+  // rows per thread are loaded up front with the tile's streams (ptr is not
+  // written by the predecessor kernel) and tested/zeroed after the tile's
+  // emits, so the slice adds no dependent DRAM round trip in front of the x
+  // gathers (C4 SpMV 102.8 -> 97.3 us; zeroing first, or after the emits
+  // without the early loads, was slower).
+  // EMPTIES == false (no empty rows in the range, rows_per_block == 0) is
+  // instantiated without the early loads and keeps the plain zeroing loop
+  // after pdl_wait: a no-op there, but without it ptxas schedules the tile
+  // code differently and matrices without empty rows lose ~9 % (C3).
+  constexpr int ZP = EMPTIES ? 2 : 0;
+  int32_t zp0[ZP > 0 ? ZP : 1], zp1[ZP > 0 ? ZP : 1];
+#pragma unroll
+  for (int k = 0; k < ZP; ++k) {
+    const int64_t r = zr0 + threadIdx.x + k * 256;
+    zp0[k] = r < zr1 ? ld_stream(C.ptr + r) : 0;
+    zp1[k] = r < zr1 ? ld_stream(C.ptr + r + 1) : 0;
+  }
+  auto zero_empty_rows_first = [&] {  // !EMPTIES only (see above)
     if (rows_per_block > 0) {
       const int64_t r0 = row_begin + blockIdx.x * rows_per_block;
       const int64_t r1 = r0 + rows_per_block < row_end ? r0 + rows_per_block : row_end;
       for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+        if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
+    }
+  };
+  auto zero_empty_rows = [&] {
+    if (EMPTIES && rows_per_block > 0) {
+      int64_t r = zr0 + threadIdx.x;
+#pragma unroll
+      for (int k = 0; k < ZP; ++k, r += 256)
+        if (r < zr1 && zp0[k] == zp1[k]) C.y[r] = 0.0;
+      for (; r < zr1; r += blockDim.x)
         if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
     }
   };
@@ -210,12 +240,12 @@ __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C,
     // the matrix loads above may overlap the previous kernel's tail (PDL);
     // x, scale and y only after it has finished
     pdl_wait();
-    zero_empty_rows();
+    if constexpr (!EMPTIES) zero_empty_rows_first();
 #pragma unroll
     for (int i = 0; i < S; ++i) v[i] *= ldx(C.x, cidx[i]);
   } else {
     pdl_wait();
-    zero_empty_rows();
+    if constexpr (!EMPTIES) zero_empty_rows_first();
   }
   if (active && tile0 + W * S > C.nnz) {
     // partial tile: every load is issued (clamped to the tile start when the
@@ -280,6 +310,7 @@ __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C,
   double right = __shfl_down_sync(0xffffffffu, rv, 1, W);
   if (j == W - 1) right = 0.0;
   if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
+  zero_empty_rows();
 }
 
 // Carry fix-up of the continuation chains (consecutive tiles whose head
@@ -331,9 +362,10 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
       generic_begin = fe;
     }
   };
-  auto warp_s_launch = [&](auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
+  auto warp_s_launch = [&](auto kern_e, auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
     const int64_t blocks = ((t_end - t_begin) * W + 255) / 256;
     const int64_t rpb = empties ? (row_end - row_begin + blocks - 1) / blocks : 0;
+    if (rpb > 0) kern = kern_e;
     launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, C, t_begin, t_end, rpb, row_begin,
                row_end);
     SPMVB_LAUNCHED("k_csr5_warp_s");
@@ -343,17 +375,17 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
   if ((sigma == 16 || sigma == 8) && (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
     if (sigma == 16) {
       switch (omega) {
-        case 32: warp_s_launch(k_csr5_warp_s<32, 16>, 32); break;
-        case 16: warp_s_launch(k_csr5_warp_s<16, 16>, 16); break;
-        case 8: warp_s_launch(k_csr5_warp_s<8, 16>, 8); break;
-        default: warp_s_launch(k_csr5_warp_s<4, 16>, 4); break;
+        case 32: warp_s_launch(k_csr5_warp_s<32, 16, true>, k_csr5_warp_s<32, 16, false>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 16, true>, k_csr5_warp_s<16, 16, false>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 16, true>, k_csr5_warp_s<8, 16, false>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 16, true>, k_csr5_warp_s<4, 16, false>, 4); break;
       }
     } else {
       switch (omega) {
-        case 32: warp_s_launch(k_csr5_warp_s<32, 8>, 32); break;
-        case 16: warp_s_launch(k_csr5_warp_s<16, 8>, 16); break;
-        case 8: warp_s_launch(k_csr5_warp_s<8, 8>, 8); break;
-        default: warp_s_launch(k_csr5_warp_s<4, 8>, 4); break;
+        case 32: warp_s_launch(k_csr5_warp_s<32, 8, true>, k_csr5_warp_s<32, 8, false>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 8, true>, k_csr5_warp_s<16, 8, false>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 8, true>, k_csr5_warp_s<8, 8, false>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 8, true>, k_csr5_warp_s<4, 8, false>, 4); break;
       }
     }
   } else if (sigma <= 1024 && (omega == 32 || omega == 16 || omega == 8 || omega == 4 || omega == 2)) {
