@@ -31,7 +31,9 @@ def main():
     ap.add_argument("--format", default="csr5")
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--cold", action="store_true", help="read a 512 MB buffer before every rep (L2 flush); median")
     a = ap.parse_args()
+    flush = torch.empty(1 << 26, dtype=torch.float64, device="cuda") if a.cold else None
     dev = torch.device("cuda", 0)
     for w in a.workloads.split(","):
         coo = build(w)
@@ -47,13 +49,26 @@ def main():
                 for _ in range(3):
                     sp.spmv(a.format, m, x, out=y)
                 torch.cuda.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(a.reps):
-                    sp.spmv(a.format, m, x, out=y)
-                e1.record()
-                torch.cuda.synchronize()
-                res[v].append(e0.elapsed_time(e1) / a.reps * 1e3)
+                if flush is not None:
+                    evs = []
+                    for _ in range(a.reps):
+                        flush.sum()
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                        sp.spmv(a.format, m, x, out=y)
+                        e1.record()
+                        evs.append((e0, e1))
+                    torch.cuda.synchronize()
+                    ts = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in evs)
+                    res[v].append(ts[len(ts) // 2])
+                else:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for _ in range(a.reps):
+                        sp.spmv(a.format, m, x, out=y)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    res[v].append(e0.elapsed_time(e1) / a.reps * 1e3)
                 if ref is None:
                     ref = y.clone()
                 elif not torch.equal(ref, y):
@@ -61,7 +76,7 @@ def main():
         nnz = m.nnz
         for v, ts in res.items():
             best = min(ts)
-            print(f"{w} {a.format} {a.var}={v}: us/SpMV {' '.join(f'{t:.1f}' for t in ts)}  best {best:.1f}"
+            print(f"{w} {a.format}{' cold' if a.cold else ''} {a.var}={v}: us/SpMV {' '.join(f'{t:.1f}' for t in ts)}  best {best:.1f}"
                   f"  {2 * nnz / best / 1e3:.1f} GFLOP/s", flush=True)
         del m, x, y, ref
         torch.cuda.empty_cache()
