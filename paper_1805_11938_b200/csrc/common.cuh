@@ -73,7 +73,8 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // The stream-ordered pool returns freed memory to the driver at every
 // synchronization by default (release threshold 0), so a conversion that
 // syncs between phases re-maps its multi-GB temporaries each call.  Keep up
-// to 16 GB cached per device (cheap against 180 GB of HBM).
+// to 32 GB cached per device (cheap against 180 GB of HBM; canonicalize of
+// the 5.3e8-entry C5 holds ~21 GB of temporaries at its peak).
 inline void pool_keep_memory() {
   static std::atomic<uint64_t> done_mask{0};
   int dev = 0;
@@ -82,7 +83,7 @@ inline void pool_keep_memory() {
   if (done_mask.load(std::memory_order_relaxed) & bit) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = 16ull << 30;
+    uint64_t thr = 32ull << 30;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done_mask.fetch_or(bit);

@@ -16,9 +16,9 @@ struct spmvb_canon {
   const void* col = nullptr;
   const double* val = nullptr;
   DevBuf<uint64_t> keys_a, keys_b;
-  DevBuf<uint32_t> vals_b, vals_s;
+  DevBuf<uint64_t> vals_a, vals_b;  // the values (bit patterns) carried through the sort
   uint64_t* skeys = nullptr;
-  uint32_t* sidx = nullptr;
+  const double* svals = nullptr;
   DevBuf<double> sums;
   DevBuf<uint8_t> keep;
   DevBuf<uint32_t> pos;
@@ -52,9 +52,10 @@ __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__
   if (__syncthreads_or(nc_any) && threadIdx.x == 0) atomicOr(noncanonical, 1);
 }
 
-__global__ void k_canon_runs(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,
-                             const double* __restrict__ val, int64_t n, double* __restrict__ sums,
-                             uint8_t* __restrict__ keep) {
+// Runs of equal keys in the sorted stream; the values were carried through
+// the (stable) sort, so each run holds its duplicates in input order.
+__global__ void k_canon_runs(const uint64_t* __restrict__ skeys, const double* __restrict__ sval, int64_t n,
+                             double* __restrict__ sums, uint8_t* __restrict__ keep) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     uint64_t k = skeys[i];
@@ -65,11 +66,11 @@ __global__ void k_canon_runs(const uint64_t* __restrict__ skeys, const uint32_t*
     }
     int64_t e = i + 1;
     while (e < n && skeys[e] == k) ++e;
-    double v0 = val[sidx[i]];
+    double v0 = sval[i];
     double s = v0;
     if (e - i > 1) {
       // numpy add.reduceat on a run: first element + pairwise(rest)
-      auto at = [&](int64_t j) { return val[sidx[j]]; };
+      auto at = [&](int64_t j) { return sval[j]; };
       s = v0 + np_pairwise(at, i + 1, e - i - 1);
     }
     sums[i] = s;
@@ -212,17 +213,18 @@ extern "C" int spmvb_canonicalize_begin(const void* row, const void* col, int in
           p->keys_a.release();
         } else {
           p->keys_b = DevBuf<uint64_t>(nnz_in, s);
-          p->vals_b = DevBuf<uint32_t>(nnz_in, s);
-          p->vals_s = DevBuf<uint32_t>(nnz_in, s);
-          RadixSortResult rs = radix_sort_pairs(p->keys_a.get(), nullptr, p->keys_b.get(), p->vals_b.get(),
-                                                p->vals_s.get(), nnz_in, rowbits + p->colbits, s);
+          p->vals_a = DevBuf<uint64_t>(nnz_in, s);
+          p->vals_b = DevBuf<uint64_t>(nnz_in, s);
+          RadixSortResult64 rs =
+              radix_sort_pairs64(p->keys_a.get(), p->keys_b.get(), reinterpret_cast<const uint64_t*>(val),
+                                 p->vals_a.get(), p->vals_b.get(), nnz_in, rowbits + p->colbits, s);
           p->skeys = rs.keys;
-          p->sidx = rs.vals;
+          p->svals = reinterpret_cast<const double*>(rs.vals);
           p->sums = DevBuf<double>(nnz_in, s);
           p->keep = DevBuf<uint8_t>(nnz_in, s);
           p->pos = DevBuf<uint32_t>(nnz_in, s);
-          k_canon_runs<<<grid_for(nnz_in, 256, 148 * 16), 256, 0, s>>>(p->skeys, p->sidx, val, nnz_in,
-                                                                       p->sums.get(), p->keep.get());
+          k_canon_runs<<<grid_for(nnz_in, 256, 148 * 16), 256, 0, s>>>(p->skeys, p->svals, nnz_in, p->sums.get(),
+                                                                       p->keep.get());
           SPMVB_LAUNCHED("k_canon_runs");
           DevBuf<uint32_t> d_total(1, s);
           const uint8_t* kp = p->keep.get();
@@ -234,9 +236,12 @@ extern "C" int spmvb_canonicalize_begin(const void* row, const void* col, int in
           SPMVB_CUDA(cudaMemcpyAsync(&h_total, d_total.get(), sizeof(h_total), cudaMemcpyDeviceToHost, s));
           SPMVB_CUDA(cudaStreamSynchronize(s));
           p->n_out = h_total;
-          // Buffers not holding the sorted keys/indices are no longer needed.
+          // The sorted values are summed into sums; buffers not holding the
+          // sorted keys are no longer needed either.
           if (p->skeys != p->keys_a.get()) p->keys_a.release(); else p->keys_b.release();
-          if (p->sidx != p->vals_b.get()) p->vals_b.release(); else p->vals_s.release();
+          p->vals_a.release();
+          p->vals_b.release();
+          p->svals = nullptr;
         }
       }
     } catch (...) {

@@ -1,6 +1,6 @@
 // Device-wide primitives used by the conversion kernels: block scans,
 // a reduce-then-scan exclusive prefix sum over integer sequences, and a
-// stable LSD radix sort of (uint64 key, uint32 value) pairs.
+// stable LSD radix sort of (uint64 key, 4- or 8-byte value) pairs.
 //
 // Everything here is integer arithmetic, so results are independent of the
 // reduction order and therefore deterministic.
@@ -241,10 +241,11 @@ void for_long_rows(Count count, int64_t n, F f, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort of (uint64 key, uint32 value) pairs over the low
-// `key_bits` bits.  8-bit digits; each pass = tile histogram, exclusive scan
-// of the digit-major histogram, and a stable tile scatter staged through
-// shared memory so global writes are coalesced per digit run.
+// Stable LSD radix sort of (uint64 key, value) pairs over the low `key_bits`
+// bits, 8-bit digits.  Below 2^30 items each pass is one kernel (digit
+// histograms of all passes from one read of the keys, then per pass a tile
+// ranking + decoupled look-back + shared-memory-staged scatter, so global
+// writes are coalesced per digit run); above, reduce-then-scan passes.
 // ---------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
@@ -257,10 +258,20 @@ struct RadixSortResult {
   uint64_t* keys;
   uint32_t* vals;
 };
+struct RadixSortResult64 {
+  uint64_t* keys;
+  uint64_t* vals;
+};
 
 // Sorts keys_a/vals_a (vals_a may be null: identity 0..n-1) using keys_b /
 // vals_b as ping-pong storage. Returns the buffers that hold the result.
 RadixSortResult radix_sort_pairs(uint64_t* keys_a, uint32_t* vals_a, uint64_t* keys_b, uint32_t* vals_b,
                                  uint32_t* vals_scratch, int64_t n, int key_bits, cudaStream_t s);
+
+// Sorts keys_a carrying 8-byte values read from vals_in (left unmodified);
+// keys_b, vals_a and vals_b are ping-pong storage.  Returns the buffers that
+// hold the result (keys_a or keys_b; vals_a or vals_b).
+RadixSortResult64 radix_sort_pairs64(uint64_t* keys_a, uint64_t* keys_b, const uint64_t* vals_in, uint64_t* vals_a,
+                                     uint64_t* vals_b, int64_t n, int key_bits, cudaStream_t s);
 
 }  // namespace spmvb

@@ -316,3 +316,23 @@ def test_extra_features_against_oracle(sp, rng):
         a = sp.canonicalize(rr, cc, vv, nr, nc)
         r, c, v = port.canonicalize(rr, cc, vv, nr, nc)
         assert sp.extract_extra_features(a) == port.extra_features(r, c, nr, nc)
+
+
+@pytest.mark.parametrize("rts", ["0", "1"])
+@pytest.mark.parametrize("shape", [(2000, 1500), (1 << 24, 3_000_017)])
+def test_canonicalize_many_tiles(sp, rng, monkeypatch, rts, shape):
+    """3M shuffled triplets (~730 radix tiles): dense duplicate runs with
+    cancellations and signed zeros on a small grid, 6-7 radix passes on a
+    large one; both sort schemes (single-pass look-back and, forced by
+    SPMVB_RADIX_RTS=1, reduce-then-scan) bit-exact against the oracle."""
+    monkeypatch.setenv("SPMVB_RADIX_RTS", rts)
+    nr, nc = shape
+    n = 3_000_000
+    rr = rng.integers(0, nr, n, dtype=np.int64)
+    cc = rng.integers(0, nc, n, dtype=np.int64)
+    vv = rng.choice([-1.5, -0.5, 0.0, -0.0, 0.25, 0.5, 1.5], size=n) + rng.integers(0, 2, n) * rng.normal(size=n)
+    a = sp.canonicalize(torch.from_numpy(rr).int().cuda(), torch.from_numpy(cc).int().cuda(),
+                        torch.from_numpy(vv).cuda(), nr, nc)
+    orow, ocol, oval = port.canonicalize(rr, cc, vv, nr, nc)
+    assert np.array_equal(np_(a.row), orow) and np.array_equal(np_(a.col), ocol)
+    assert same_bits(a.data, oval)
