@@ -19,9 +19,7 @@ struct spmvb_canon {
   DevBuf<uint64_t> vals_a, vals_b;  // the values (bit patterns) carried through the sort
   uint64_t* skeys = nullptr;
   const double* svals = nullptr;
-  DevBuf<double> sums;
-  DevBuf<uint8_t> keep;
-  DevBuf<uint32_t> pos;
+  DevBuf<uint32_t> tile_off;  // kept runs before each compaction tile
 };
 
 namespace {
@@ -31,66 +29,139 @@ __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__
                                 int64_t n, int64_t n_rows, int64_t n_cols, int colbits, uint64_t* __restrict__ keys,
                                 unsigned long long* bad, int* noncanonical) {
   // flags are reduced per block before touching global memory: unsorted
-  // input would otherwise put one atomic per entry on a single address
+  // input would otherwise put one atomic per entry on a single address.
+  // U warp-contiguous groups per thread are loaded before any is used; the
+  // previous entry comes from the neighbouring lane (lane 0 loads it).
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int nc_any = 0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t r = static_cast<int64_t>(row[i]);
-    int64_t c = static_cast<int64_t>(col[i]);
-    bool oob = r < 0 || r >= n_rows || c < 0 || c >= n_cols;
-    uint64_t key = oob ? 0ull : ((static_cast<uint64_t>(r) << colbits) | static_cast<uint64_t>(c));
-    keys[i] = key;
-    if (oob) atomicMin(bad, static_cast<unsigned long long>(i));  // rare: any out-of-range entry aborts
-    bool nc = (val[i] == 0.0);
-    if (i > 0 && !oob) {
-      int64_t pr = static_cast<int64_t>(row[i - 1]);
-      int64_t pc = static_cast<int64_t>(col[i - 1]);
-      if (pr > r || (pr == r && pc >= c)) nc = true;
+  for (int64_t wb = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31); wb < n; wb += U * stride) {
+    int64_t r[U], c[U], pr[U], pc[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = wb + u * stride + lane;
+      const bool ok = i < n;
+      r[u] = ok ? static_cast<int64_t>(row[i]) : 0;
+      c[u] = ok ? static_cast<int64_t>(col[i]) : 0;
+      v[u] = ok ? val[i] : 1.0;
+      const bool first = lane == 0 && ok && i > 0;
+      pr[u] = first ? static_cast<int64_t>(row[i - 1]) : 0;
+      pc[u] = first ? static_cast<int64_t>(col[i - 1]) : 0;
     }
-    nc_any |= nc ? 1 : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = wb + u * stride + lane;
+      const int64_t ur = __shfl_up_sync(0xffffffffu, r[u], 1), uc = __shfl_up_sync(0xffffffffu, c[u], 1);
+      if (lane > 0) {
+        pr[u] = ur;
+        pc[u] = uc;
+      }
+      if (i >= n) continue;
+      const bool oob = r[u] < 0 || r[u] >= n_rows || c[u] < 0 || c[u] >= n_cols;
+      keys[i] = oob ? 0ull : ((static_cast<uint64_t>(r[u]) << colbits) | static_cast<uint64_t>(c[u]));
+      if (oob) atomicMin(bad, static_cast<unsigned long long>(i));  // rare: any out-of-range entry aborts
+      bool nc = (v[u] == 0.0);
+      if (i > 0 && !oob && (pr[u] > r[u] || (pr[u] == r[u] && pc[u] >= c[u]))) nc = true;
+      nc_any |= nc ? 1 : 0;
+    }
   }
   if (__syncthreads_or(nc_any) && threadIdx.x == 0) atomicOr(noncanonical, 1);
 }
 
 // Runs of equal keys in the sorted stream; the values were carried through
-// the (stable) sort, so each run holds its duplicates in input order.
-__global__ void k_canon_runs(const uint64_t* __restrict__ skeys, const double* __restrict__ sval, int64_t n,
-                             double* __restrict__ sums, uint8_t* __restrict__ keep) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    uint64_t k = skeys[i];
-    bool head = (i == 0) || (skeys[i - 1] != k);
-    if (!head) {
-      keep[i] = 0;
-      continue;
-    }
-    int64_t e = i + 1;
-    while (e < n && skeys[e] == k) ++e;
-    double v0 = sval[i];
-    double s = v0;
-    if (e - i > 1) {
-      // numpy add.reduceat on a run: first element + pairwise(rest)
-      auto at = [&](int64_t j) { return sval[j]; };
-      s = v0 + np_pairwise(at, i + 1, e - i - 1);
-    }
-    sums[i] = s;
-    keep[i] = (s != 0.0) ? 1 : 0;  // NaN != 0.0: kept, as in coo.py:124
-  }
+// the (stable) sort, so each run holds its duplicates in input order.  A run
+// is reduced by the item at its head: numpy add.reduceat = first element +
+// pairwise(rest) (coo.py:123); the run is kept iff that sum != 0.0 (NaN
+// kept, coo.py:124).  Rare (duplicates), so out of line.
+__device__ __noinline__ double canon_run_sum(const uint64_t* __restrict__ skeys, const double* __restrict__ sval,
+                                             int64_t i, int64_t n) {
+  const uint64_t k = skeys[i];
+  int64_t e = i + 2;
+  while (e < n && skeys[e] == k) ++e;
+  auto at = [&](int64_t j) { return sval[j]; };
+  return sval[i] + np_pairwise(at, i + 1, e - i - 1);
 }
 
-__global__ void k_canon_emit(const uint64_t* __restrict__ skeys, const double* __restrict__ sums,
-                             const uint8_t* __restrict__ keep, const uint32_t* __restrict__ pos, int64_t n,
-                             int colbits, int32_t* __restrict__ row_out, int32_t* __restrict__ col_out,
-                             double* __restrict__ val_out) {
-  const uint64_t mask = (colbits >= 64) ? ~0ull : ((1ull << colbits) - 1ull);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (!keep[i]) continue;
-    uint64_t k = skeys[i];
-    uint32_t p = pos[i];
-    row_out[p] = static_cast<int32_t>(k >> colbits);
-    col_out[p] = static_cast<int32_t>(k & mask);
-    val_out[p] = sums[i];
+// One tile of CANON_TILE sorted items per block; warp w owns the contiguous
+// items [w*32*CANON_STEPS, (w+1)*32*CANON_STEPS) of the tile, 32 per step.  COUNT: the tile's
+// number of kept runs -> tile_cnt[b].  !COUNT: the kept runs are written at
+// tile_off[b] + (their rank among the tile's kept runs) -- a compaction whose
+// offsets come from the scan of the counts (so canonicalize needs no
+// per-item sums/flags/positions arrays).
+constexpr int CANON_THREADS = 256;
+constexpr int CANON_STEPS = 8;
+constexpr int64_t CANON_TILE = CANON_THREADS * CANON_STEPS;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(CANON_THREADS, 4) k_canon_compact(const uint64_t* __restrict__ skeys,
+                                                                  const double* __restrict__ sval, int64_t n,
+                                                                  uint32_t* __restrict__ tile_cnt,
+                                                                  const uint32_t* __restrict__ tile_off, int colbits,
+                                                                  int32_t* __restrict__ row_out,
+                                                                  int32_t* __restrict__ col_out,
+                                                                  double* __restrict__ val_out) {
+  __shared__ uint32_t wsum[CANON_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = blockIdx.x * CANON_TILE + static_cast<int64_t>(warp) * (32 * CANON_STEPS);
+  uint64_t key[CANON_STEPS];
+  double sum[CANON_STEPS];
+  uint32_t keep = 0;  // bit r: item of step r starts a kept run
+#pragma unroll
+  for (int r = 0; r < CANON_STEPS; ++r) {
+    const int64_t i = base + r * 32 + lane;
+    key[r] = i < n ? skeys[i] : 0;
+    sum[r] = i < n ? sval[i] : 0.0;
+  }
+  // keys just before and just after this warp's items
+  const int64_t after = base + 32 * CANON_STEPS;
+  uint64_t before_key = 0, after_key = ~0ull;
+  if (lane == 0 && base > 0 && base - 1 < n) before_key = skeys[base - 1];
+  if (lane == 31 && after < n) after_key = skeys[after];
+#pragma unroll
+  for (int r = 0; r < CANON_STEPS; ++r) {
+    const int64_t i = base + r * 32 + lane;
+    uint64_t prev = __shfl_up_sync(0xffffffffu, key[r], 1);
+    const uint64_t first_next = __shfl_sync(0xffffffffu, r + 1 < CANON_STEPS ? key[r + 1 < CANON_STEPS ? r + 1 : r] : 0, 0);
+    uint64_t next = __shfl_down_sync(0xffffffffu, key[r], 1);
+    if (lane == 0) prev = before_key;
+    if (lane == 31) next = r + 1 < CANON_STEPS ? first_next : after_key;
+    before_key = __shfl_sync(0xffffffffu, key[r], 31);  // lane 0's prev in the next step
+    if (i < n && (i == 0 || prev != key[r])) {
+      if (i + 1 < n && next == key[r]) sum[r] = canon_run_sum(skeys, sval, i, n);
+      if (sum[r] != 0.0) keep |= 1u << r;
+    }
+  }
+  // kept runs of this warp, of the warps before it, of the tiles before
+  uint32_t wcount = 0;
+#pragma unroll
+  for (int r = 0; r < CANON_STEPS; ++r) wcount += __popc(__ballot_sync(0xffffffffu, (keep >> r) & 1u));
+  if (lane == 0) wsum[warp] = wcount;
+  __syncthreads();
+  if (COUNT) {
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < CANON_THREADS / 32; ++w) t += wsum[w];
+      tile_cnt[blockIdx.x] = t;
+    }
+    return;
+  }
+  uint32_t pos = tile_off[blockIdx.x];
+  for (int w = 0; w < warp; ++w) pos += wsum[w];
+  const uint64_t cmask = (colbits >= 64) ? ~0ull : ((1ull << colbits) - 1ull);
+#pragma unroll
+  for (int r = 0; r < CANON_STEPS; ++r) {
+    const bool kp = (keep >> r) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, kp);
+    if (kp) {
+      const uint32_t p = pos + __popc(bal & lanemask_lt());
+      row_out[p] = static_cast<int32_t>(key[r] >> colbits);
+      col_out[p] = static_cast<int32_t>(key[r] & cmask);
+      val_out[p] = sum[r];
+    }
+    pos += __popc(bal);
   }
 }
 
@@ -215,33 +286,27 @@ extern "C" int spmvb_canonicalize_begin(const void* row, const void* col, int in
           p->keys_b = DevBuf<uint64_t>(nnz_in, s);
           p->vals_a = DevBuf<uint64_t>(nnz_in, s);
           p->vals_b = DevBuf<uint64_t>(nnz_in, s);
+          uint32_t h_total = 0;
           RadixSortResult64 rs =
               radix_sort_pairs64(p->keys_a.get(), p->keys_b.get(), reinterpret_cast<const uint64_t*>(val),
                                  p->vals_a.get(), p->vals_b.get(), nnz_in, rowbits + p->colbits, s);
           p->skeys = rs.keys;
           p->svals = reinterpret_cast<const double*>(rs.vals);
-          p->sums = DevBuf<double>(nnz_in, s);
-          p->keep = DevBuf<uint8_t>(nnz_in, s);
-          p->pos = DevBuf<uint32_t>(nnz_in, s);
-          k_canon_runs<<<grid_for(nnz_in, 256, 148 * 16), 256, 0, s>>>(p->skeys, p->svals, nnz_in, p->sums.get(),
-                                                                       p->keep.get());
-          SPMVB_LAUNCHED("k_canon_runs");
-          DevBuf<uint32_t> d_total(1, s);
-          const uint8_t* kp = p->keep.get();
-          uint32_t* pp = p->pos.get();
-          exclusive_scan<uint32_t>(
-              nnz_in, [=] __device__(int64_t i) { return static_cast<uint32_t>(kp[i]); },
-              ArrayStore<uint32_t>{pp}, OpSum{}, 0u, d_total.get(), s);
-          uint32_t h_total = 0;
-          SPMVB_CUDA(cudaMemcpyAsync(&h_total, d_total.get(), sizeof(h_total), cudaMemcpyDeviceToHost, s));
-          SPMVB_CUDA(cudaStreamSynchronize(s));
+          const int64_t tiles = (nnz_in + CANON_TILE - 1) / CANON_TILE;
+          p->tile_off = DevBuf<uint32_t>(tiles, s);
+          {
+            DevBuf<uint32_t> cnt(tiles, s), d_total(1, s);
+            k_canon_compact<true><<<static_cast<unsigned>(tiles), CANON_THREADS, 0, s>>>(
+                p->skeys, p->svals, nnz_in, cnt.get(), nullptr, 0, nullptr, nullptr, nullptr);
+            SPMVB_LAUNCHED("k_canon_compact");
+            exclusive_scan<uint32_t>(tiles, ArrayLoad<uint32_t>{cnt.get()}, ArrayStore<uint32_t>{p->tile_off.get()},
+                                     OpSum{}, 0u, d_total.get(), s);
+            copy_to_host(&h_total, d_total.get(), 1, s);
+          }
           p->n_out = h_total;
-          // The sorted values are summed into sums; buffers not holding the
-          // sorted keys are no longer needed either.
+          // buffers not holding the sorted keys/values are no longer needed
           if (p->skeys != p->keys_a.get()) p->keys_a.release(); else p->keys_b.release();
-          p->vals_a.release();
-          p->vals_b.release();
-          p->svals = nullptr;
+          if (p->svals != reinterpret_cast<const double*>(p->vals_a.get())) p->vals_a.release(); else p->vals_b.release();
         }
       }
     } catch (...) {
@@ -271,9 +336,10 @@ extern "C" int spmvb_canonicalize_finish(spmvb_canon* p, int32_t* row_out, int32
                                                    col_out, val_out);
         SPMVB_LAUNCHED("k_narrow_copy");
       } else {
-        k_canon_emit<<<g, 256, 0, s>>>(p->skeys, p->sums.get(), p->keep.get(), p->pos.get(), p->n_in, p->colbits,
-                                       row_out, col_out, val_out);
-        SPMVB_LAUNCHED("k_canon_emit");
+        const int64_t tiles = (p->n_in + CANON_TILE - 1) / CANON_TILE;
+        k_canon_compact<false><<<static_cast<unsigned>(tiles), CANON_THREADS, 0, s>>>(
+            p->skeys, p->svals, p->n_in, nullptr, p->tile_off.get(), p->colbits, row_out, col_out, val_out);
+        SPMVB_LAUNCHED("k_canon_compact");
       }
     }
     delete p;
