@@ -35,17 +35,57 @@ __global__ void k_mark_row_starts(const int32_t* __restrict__ ptr, int64_t n_row
   }
 }
 
-__global__ void k_csr5_scatter(int64_t nnz, int64_t tile, int64_t sigma, const uint8_t* __restrict__ flags_csr,
-                               const int32_t* __restrict__ col, const double* __restrict__ val,
-                               uint8_t* __restrict__ bit_flag, int32_t* __restrict__ col_out,
-                               double* __restrict__ val_out) {
-  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+__global__ void k_csr5_scatter(int64_t k0, int64_t nnz, int64_t tile, int64_t sigma,
+                               const uint8_t* __restrict__ flags_csr, const int32_t* __restrict__ col,
+                               const double* __restrict__ val, uint8_t* __restrict__ bit_flag,
+                               int32_t* __restrict__ col_out, double* __restrict__ val_out) {
+  for (int64_t k = k0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t s = csr5_stored(k, tile, sigma, nnz);
     bool head = (k % tile) == 0;
     bit_flag[s] = (flags_csr[k] || head) ? 1 : 0;
     col_out[s] = col[k];
     val_out[s] = val[k];
+  }
+}
+
+// Full tiles (tile = omega*sigma <= CSR5_SMEM_TILE entries): one tile per
+// block iteration, read in CSR order (coalesced), transposed to the stored
+// order (sigma x omega grid, row-major; formats.py:204-209) in shared memory
+// and written out coalesced.  32-bit in-tile arithmetic.
+constexpr int CSR5_SMEM_TILE = 4096;
+__global__ void __launch_bounds__(256) k_csr5_scatter_tiles(int64_t full_tiles, int tile, int omega, int sigma,
+                                                            const uint8_t* __restrict__ flags_csr,
+                                                            const int32_t* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            uint8_t* __restrict__ bit_flag,
+                                                            int32_t* __restrict__ col_out,
+                                                            double* __restrict__ val_out) {
+  // stored slot st lives at st + st/32 (one pad word per 32: the transposed
+  // writes of a warp then fall in distinct banks)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int padded = tile + tile / 32 + 1;
+  double* sv = reinterpret_cast<double*>(smem_raw);
+  int32_t* sc = reinterpret_cast<int32_t*>(sv + padded);
+  uint8_t* sf = reinterpret_cast<uint8_t*>(sc + padded);
+  for (int64_t t = blockIdx.x; t < full_tiles; t += gridDim.x) {
+    const int64_t base = t * tile;
+    for (int p = threadIdx.x; p < tile; p += blockDim.x) {
+      const int gi = p % sigma, gj = p / sigma;
+      const int st = gi * omega + gj;
+      const int sp = st + (st >> 5);
+      sv[sp] = val[base + p];
+      sc[sp] = col[base + p];
+      sf[sp] = (p == 0 || flags_csr[base + p]) ? 1 : 0;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < tile; p += blockDim.x) {
+      const int sp = p + (p >> 5);
+      val_out[base + p] = sv[sp];
+      col_out[base + p] = sc[sp];
+      bit_flag[base + p] = sf[sp];
+    }
+    __syncthreads();
   }
 }
 
@@ -278,9 +318,22 @@ void csr5_build(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* 
   SPMVB_CUDA(cudaMemsetAsync(flags.get(), 0, nnz, s));
   k_mark_row_starts<<<grid_for(n_rows, 256, 148 * 16), 256, 0, s>>>(ptr, n_rows, flags.get());
   SPMVB_LAUNCHED("k_mark_row_starts");
-  k_csr5_scatter<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(nnz, tile, sigma, flags.get(), col, val, bit_flag,
-                                                              col_out, val_out);
-  SPMVB_LAUNCHED("k_csr5_scatter");
+  int64_t scatter_from = 0;  // entries before this went through the shared-memory transpose
+  if (tile <= CSR5_SMEM_TILE && nnz / tile > 0) {
+    const int64_t full = nnz / tile;
+    const size_t smem = static_cast<size_t>(tile + tile / 32 + 1) * (sizeof(double) + sizeof(int32_t) + 1);
+    SPMVB_CUDA(cudaFuncSetAttribute(k_csr5_scatter_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_csr5_scatter_tiles<<<grid_for(full, 1, 148 * 8), 256, smem, s>>>(full, static_cast<int>(tile), omega, sigma,
+                                                                        flags.get(), col, val, bit_flag, col_out,
+                                                                        val_out);
+    SPMVB_LAUNCHED("k_csr5_scatter_tiles");
+    scatter_from = full * tile;
+  }
+  if (scatter_from < nnz) {
+    k_csr5_scatter<<<grid_for(nnz - scatter_from, 256, 148 * 16), 256, 0, s>>>(
+        scatter_from, nnz, tile, sigma, flags.get(), col, val, bit_flag, col_out, val_out);
+    SPMVB_LAUNCHED("k_csr5_scatter");
+  }
   // nz_rank[r] = number of non-empty rows before r
   DevBuf<int32_t> nz_rank(n_rows > 0 ? n_rows : 1, s);
   int32_t* nr = nz_rank.get();
