@@ -141,6 +141,49 @@ __global__ void k_csr5_descriptor(int64_t nnz, int64_t num_tiles, int omega, int
   }
 }
 
+// omega <= 32: one warp per tile, lane j = tile column j (coalesced flag
+// reads and descriptor writes; seg_off from a ballot of the unflagged tops).
+__global__ void k_csr5_descriptor_warp(int64_t nnz, int64_t num_tiles, int omega, int sigma,
+                                       const uint8_t* __restrict__ flags_csr, const int32_t* __restrict__ ptr,
+                                       const int32_t* __restrict__ tile_ptr, const int32_t* __restrict__ nz_rank,
+                                       int32_t* __restrict__ y_off, int32_t* __restrict__ seg_off,
+                                       uint32_t* __restrict__ tile_aux) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = static_cast<int64_t>(omega) * sigma;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t t = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; t < num_tiles; t += nwarps) {
+    const int64_t base = t * tile;
+    const int64_t m = nnz - base < tile ? nnz - base : tile;
+    const bool active = lane < omega;
+    const int64_t lo = static_cast<int64_t>(lane) * sigma;
+    const int64_t hi = lo + sigma < m ? lo + sigma : m;
+    int32_t cnt = 0;
+    if (active)
+      for (int64_t q = lo; q < hi; ++q) cnt += (flags_csr[base + q] || q == 0) ? 1 : 0;
+    int32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const bool unflagged_top = active && lo < m && !(flags_csr[base + lo] || lo == 0);
+    const unsigned tops = __ballot_sync(0xffffffffu, unflagged_top);
+    // columns lane+1, lane+2, ... with an unflagged top, up to the first one without
+    const unsigned above = lane == 31 ? 0u : tops >> (lane + 1);
+    const int32_t spill = (~above == 0u) ? 31 - lane : __ffs(~above) - 1;
+    if (active) {
+      y_off[t * omega + lane] = incl - cnt;
+      seg_off[t * omega + lane] = spill;
+    }
+    if (lane == 0) {
+      const int32_t r = tile_ptr[t];
+      const bool cont = ptr[r] < base;  // head entry continues a row that began earlier
+      const uint32_t rank = nz_rank ? static_cast<uint32_t>(nz_rank[r]) : static_cast<uint32_t>(r);
+      tile_aux[t] = rank | (cont ? 0x80000000u : 0u);
+    }
+  }
+}
+
 // ------------------------------------------------------------------- ELL --
 __global__ void k_ell_fill(int64_t n_rows, int64_t k, const int32_t* __restrict__ ptr,
                            const int32_t* __restrict__ col, const double* __restrict__ val, int32_t* __restrict__ idx_out,
@@ -340,9 +383,15 @@ void csr5_build(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* 
   exclusive_scan<int32_t>(
       n_rows, [=] __device__(int64_t i) { return ptr[i + 1] > ptr[i] ? 1 : 0; }, ArrayStore<int32_t>{nr}, OpSum{},
       0, static_cast<int32_t*>(nullptr), s);
-  k_csr5_descriptor<<<grid_for(num_tiles, 128, 148 * 64), 128, 0, s>>>(nnz, num_tiles, omega, sigma, flags.get(), ptr,
-                                                                      tile_ptr, nr, y_off, seg_off, tile_aux);
-  SPMVB_LAUNCHED("k_csr5_descriptor");
+  if (omega <= 32) {
+    k_csr5_descriptor_warp<<<grid_for(num_tiles * 32, 256, 148 * 16), 256, 0, s>>>(
+        nnz, num_tiles, omega, sigma, flags.get(), ptr, tile_ptr, nr, y_off, seg_off, tile_aux);
+    SPMVB_LAUNCHED("k_csr5_descriptor_warp");
+  } else {
+    k_csr5_descriptor<<<grid_for(num_tiles, 128, 148 * 64), 128, 0, s>>>(nnz, num_tiles, omega, sigma, flags.get(),
+                                                                        ptr, tile_ptr, nr, y_off, seg_off, tile_aux);
+    SPMVB_LAUNCHED("k_csr5_descriptor");
+  }
 }
 
 }  // namespace
