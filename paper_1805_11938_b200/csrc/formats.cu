@@ -234,23 +234,72 @@ __global__ void k_sell_widths(const int64_t* __restrict__ row_nnz_perm, int64_t 
   }
 }
 
+// Thread per permuted row over its slice's column-major grid; rows of wide
+// slices (the plan's wide list) are left to k_sell_fill_wide.
 __global__ void k_sell_fill(int64_t n_rows, int64_t c, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                             const double* __restrict__ val, const int32_t* __restrict__ perm,
                             const int64_t* __restrict__ widths, const int64_t* __restrict__ slice_off,
-                            int32_t* __restrict__ idx_out, double* __restrict__ val_out) {
+                            int32_t* __restrict__ idx_out, double* __restrict__ val_out, bool skip_wide) {
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n_rows;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = p / c, local = p - s * c;
     const int64_t rows_s = (s + 1) * c <= n_rows ? c : n_rows - s * c;
+    const int64_t w = widths[s], base = slice_off[s];
+    if (skip_wide && w > SPMVB_SELL_WIDE_COLS && rows_s <= 128) continue;
     const int32_t r = perm[p];
     const int32_t a = ptr[r], b = ptr[r + 1];
     const int64_t cnt = b - a;
     const int32_t last = cnt ? col[b - 1] : 0;
-    const int64_t w = widths[s], base = slice_off[s];
     for (int64_t j = 0; j < w; ++j) {
       bool real = j < cnt;
       idx_out[base + j * rows_s + local] = real ? col[a + j] : last;
       val_out[base + j * rows_s + local] = real ? val[a + j] : 0.0;
+    }
+  }
+}
+
+// Wide slices (power-law rows: one thread per row would walk up to ~4e5
+// columns serially): one CTA per piece of ~32K cells, cells in storage order
+// (coalesced writes), the slice's rows staged in shared memory.
+__global__ void __launch_bounds__(256) k_sell_fill_wide(int64_t n_rows, int64_t c, const int32_t* __restrict__ ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const double* __restrict__ val,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int64_t* __restrict__ widths,
+                                                        const int64_t* __restrict__ slice_off,
+                                                        const int32_t* __restrict__ wide, int64_t n_wide,
+                                                        const int32_t* __restrict__ first_piece, int64_t n_pieces,
+                                                        int32_t* __restrict__ idx_out, double* __restrict__ val_out) {
+  __shared__ int32_t ra[128], rc[128], rl[128];  // row start, count, last column
+  for (int64_t item = blockIdx.x; item < n_pieces; item += gridDim.x) {
+    int64_t lo = 0, hi = n_wide - 1;  // wide slice of this piece: last i with first_piece[i] <= item
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (first_piece[mid] <= item) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t sl = wide[lo];
+    const int rows_s = sell_rows(sl, c, n_rows);
+    const int64_t pc = sell_piece_cols(rows_s);
+    const int64_t w = widths[sl];
+    const int64_t j0 = (item - first_piece[lo]) * pc;
+    const int64_t j1 = j0 + pc < w ? j0 + pc : w;
+    __syncthreads();  // previous piece done with the row table
+    if (threadIdx.x < rows_s) {
+      const int32_t r = perm[sl * c + threadIdx.x];
+      const int32_t a = ptr[r], b = ptr[r + 1];
+      ra[threadIdx.x] = a;
+      rc[threadIdx.x] = b - a;
+      rl[threadIdx.x] = b > a ? col[b - 1] : 0;
+    }
+    __syncthreads();
+    const int64_t base = slice_off[sl];
+    for (int64_t e = j0 * rows_s + threadIdx.x; e < j1 * rows_s; e += blockDim.x) {
+      const int64_t j = e / rows_s;
+      const int l = static_cast<int>(e - j * rows_s);
+      const bool real = j < rc[l];
+      idx_out[base + e] = real ? col[ra[l] + j] : rl[l];
+      val_out[base + e] = real ? val[ra[l] + j] : 0.0;
     }
   }
 }
@@ -282,11 +331,10 @@ struct ArrCount {
   __device__ int64_t operator()(int64_t r) const { return c[r]; }
 };
 
-__global__ void k_hyb_fill(int64_t n_rows, int64_t k, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                           const double* __restrict__ val, const int32_t* __restrict__ tail_ptr,
-                           int32_t* __restrict__ ell_idx, double* __restrict__ ell_val,
-                           int64_t* __restrict__ ell_row_nnz, int32_t* __restrict__ tail_row,
-                           int32_t* __restrict__ tail_col, double* __restrict__ tail_val) {
+// ELL part: thread per row, column-major slots (coalesced).
+__global__ void k_hyb_ell(int64_t n_rows, int64_t k, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                          const double* __restrict__ val, int32_t* __restrict__ ell_idx, double* __restrict__ ell_val,
+                          int64_t* __restrict__ ell_row_nnz) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t a = ptr[r], b = ptr[r + 1];
@@ -299,12 +347,53 @@ __global__ void k_hyb_fill(int64_t n_rows, int64_t k, const int32_t* __restrict_
       ell_val[j * n_rows + r] = real ? val[a + j] : 0.0;
     }
     ell_row_nnz[r] = kept;
-    if (cnt > LONG_ROW) continue;  // tail copied by a whole CTA (spmvb_hyb_fill)
-    const int64_t t0 = tail_ptr[r];
-    for (int64_t j = kept; j < cnt; ++j) {
-      tail_row[t0 + j - kept] = static_cast<int32_t>(r);
-      tail_col[t0 + j - kept] = col[a + j];
-      tail_val[t0 + j - kept] = val[a + j];
+  }
+}
+
+// COO tail: one warp per 32 consecutive rows, their tail entries copied as
+// one lane-strided stream (coalesced reads and writes even for short rows);
+// output position -> row by a 5-step shuffle search over the warp's rows.
+// Rows longer than LONG_ROW are left to a CTA each (spmvb_hyb_fill).
+__global__ void k_hyb_tail(int64_t n_rows, int64_t k, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                           const double* __restrict__ val, const int32_t* __restrict__ tail_ptr,
+                           int32_t* __restrict__ tail_row, int32_t* __restrict__ tail_col,
+                           double* __restrict__ tail_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r0 = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * 32; r0 < n_rows;
+       r0 += nwarps * 32) {
+    const int64_t r = r0 + lane;
+    int32_t len = 0, src = 0, dst = 0;
+    if (r < n_rows) {
+      const int32_t a = ptr[r], cnt = ptr[r + 1] - a;
+      len = (cnt > k && cnt <= LONG_ROW) ? static_cast<int32_t>(cnt - k) : 0;
+      src = a + static_cast<int32_t>(k);
+      dst = tail_ptr[r];
+    }
+    int32_t incl = len;  // inclusive prefix of the warp's stream lengths
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int32_t q0 = 0; q0 < total; q0 += 32) {
+      const int32_t q = q0 + lane;
+      // row of stream position q: the first lane whose inclusive prefix exceeds q
+      int l = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int32_t v = __shfl_sync(0xffffffffu, incl, l + step - 1);
+        if (v <= q) l += step;
+      }
+      const int32_t start = __shfl_sync(0xffffffffu, incl - len, l);
+      const int32_t s_l = __shfl_sync(0xffffffffu, src, l), d_l = __shfl_sync(0xffffffffu, dst, l);
+      if (q < total) {
+        const int32_t off = q - start;
+        tail_row[d_l + off] = static_cast<int32_t>(r0 + l);
+        tail_col[d_l + off] = col[s_l + off];
+        tail_val[d_l + off] = val[s_l + off];
+      }
     }
   }
 }
@@ -485,9 +574,23 @@ extern "C" int spmvb_sell_fill(int64_t n_rows, const int32_t* ptr, const int32_t
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
+    const int64_t n_slices = (n_rows + c - 1) / c;
+    DevBuf<int32_t> wide(n_slices, s), first_piece(n_slices, s);
+    int64_t n_wide = 0, n_pieces = 0;
+    if (const int st = spmvb_sell_wide_plan(n_rows, c, widths, wide.get(), &n_wide, nullptr, first_piece.get(),
+                                            &n_pieces, s)) {
+      const std::string msg = spmvb_last_error();
+      fail(st, "%s", msg.c_str());
+    }
     k_sell_fill<<<grid_for(n_rows, 256, 148 * 64), 256, 0, s>>>(n_rows, c, ptr, col, val, perm, widths, slice_off,
-                                                                idx_out, val_out);
+                                                                idx_out, val_out, n_wide > 0);
     SPMVB_LAUNCHED("k_sell_fill");
+    if (n_wide > 0 && n_pieces > 0) {
+      k_sell_fill_wide<<<grid_for(n_pieces, 1, 148 * 8), 256, 0, s>>>(n_rows, c, ptr, col, val, perm, widths,
+                                                                        slice_off, wide.get(), n_wide,
+                                                                        first_piece.get(), n_pieces, idx_out, val_out);
+      SPMVB_LAUNCHED("k_sell_fill_wide");
+    }
   });
 }
 
@@ -527,9 +630,12 @@ extern "C" int spmvb_hyb_fill(int64_t n_rows, const int32_t* ptr, const int32_t*
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
-    k_hyb_fill<<<grid_for(n_rows, 256, 148 * 64), 256, 0, s>>>(n_rows, k, ptr, col, val, tail_ptr, ell_idx, ell_val,
-                                                               ell_row_nnz, tail_row, tail_col, tail_val);
-    SPMVB_LAUNCHED("k_hyb_fill");
+    k_hyb_ell<<<grid_for(n_rows, 256, 148 * 64), 256, 0, s>>>(n_rows, k, ptr, col, val, ell_idx, ell_val,
+                                                              ell_row_nnz);
+    SPMVB_LAUNCHED("k_hyb_ell");
+    k_hyb_tail<<<grid_for((n_rows + 31) / 32 * 32, 256, 148 * 64), 256, 0, s>>>(n_rows, k, ptr, col, val, tail_ptr,
+                                                                                 tail_row, tail_col, tail_val);
+    SPMVB_LAUNCHED("k_hyb_tail");
     for_long_rows(
         [=] __device__(int64_t r) { return static_cast<int64_t>(ptr[r + 1] - ptr[r]); }, n_rows,
         [=] __device__(int64_t r, int64_t first, int64_t stride) {

@@ -59,17 +59,7 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE == 2 ? 5 : 4)) k_sp
 // Deterministic; not the reference's sequential order, so within tolerance
 // rather than bit-exact.  (One CTA per whole slice serialised the widest
 // R-MAT slices: 33 ms of a C5 SELL SpMV.)
-constexpr int64_t SELL_PIECE_CELLS = 32768;
 constexpr int SELL_PART_STRIDE = 128;  // partial slots per piece (max rows of a wide slice)
-
-__device__ __forceinline__ int64_t sell_piece_cols(int rows_s) {
-  const int64_t pc = SELL_PIECE_CELLS / rows_s;
-  return pc < 256 ? 256 : pc;
-}
-
-__device__ __forceinline__ int sell_rows(int64_t sl, int64_t c, int64_t n_rows) {
-  return static_cast<int>((sl + 1) * c <= n_rows ? c : n_rows - sl * c);
-}
 
 // pieces per wide slice
 __global__ void k_sell_wide_pieces(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
