@@ -114,6 +114,7 @@ def test_config_parity(sp, name):
         assert np.array_equal(h(ms.perm), so.perm) and np.array_equal(h(ms.widths), so.widths)
         flat = np.concatenate([d.ravel(order="F") for d in so.data])
         assert h(ms.flat_data).tobytes() == flat.tobytes()
+        assert np.array_equal(h(ms.flat_indices), so.flat_indices)
         ys = sp.spmv("sell", ms, xd)
         if int(so.widths.max()) <= 256:  # every slice summed sequentially: bit-identical
             assert h(ys).tobytes() == port.spmv_sell(so, n, x).tobytes()

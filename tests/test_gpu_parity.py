@@ -336,3 +336,37 @@ def test_canonicalize_many_tiles(sp, rng, monkeypatch, rts, shape):
     orow, ocol, oval = port.canonicalize(rr, cc, vv, nr, nc)
     assert np.array_equal(np_(a.row), orow) and np.array_equal(np_(a.col), ocol)
     assert same_bits(a.data, oval)
+
+
+def test_wide_rows_sell_hyb(sp, rng):
+    """Rows far wider than the SELL wide-slice threshold (256 columns) and
+    the per-row copy limit (LONG_ROW = 512) next to short and empty rows:
+    SELL grids (flat storage, several c/sigma) and the HYB ELL part and tail
+    bit-exact against the oracle; SpMV within tolerance."""
+    n, nc = 700, 6000
+    rows, cols = [], []
+    for r in range(n):
+        k = int(rng.integers(600, 3000)) if r % 97 == 5 else int(rng.integers(0, 12))
+        cs = np.sort(rng.choice(nc, size=k, replace=False))
+        rows.append(np.full(k, r)); cols.append(cs)
+    rr, cc = np.concatenate(rows), np.concatenate(cols)
+    vv = rng.normal(size=rr.size)
+    a = sp.canonicalize(torch.from_numpy(rr).int(), torch.from_numpy(cc).int(), vv, n, nc)
+    orow, ocol, oval = port.canonicalize(rr, cc, vv, n, nc)
+    optr, oind, odat = port.to_csr(orow, ocol, oval, n)
+    x = rng.normal(size=nc)
+    ref = port.dense_spmv_oracle(orow, ocol, oval, n, x)
+    bound = port.dense_spmv_oracle(orow, ocol, np.abs(oval), n, np.abs(x))
+    for c_, s_ in [(4, 0), (32, 0), (32, 64), (100, 0), (7, 7 * 20)]:
+        so = port.to_sell(optr, oind, odat, n, c_, s_, max_cells=1 << 30)
+        ms = sp.to_sell(a, c_, s_, max_cells=1 << 30)
+        assert np.array_equal(np_(ms.perm), so.perm) and np.array_equal(np_(ms.widths), so.widths)
+        assert np.array_equal(np_(ms.flat_indices), so.flat_indices), (c_, s_)
+        assert np_(ms.flat_data).tobytes() == so.flat_data.tobytes(), (c_, s_)
+        assert_within(sp.spmv("sell", ms, x), ref, bound)
+    K, hi, hd, hn, tail = port.to_hyb(orow, ocol, oval, n)
+    mh = sp.to_hyb(a)
+    assert mh.k == K and np.array_equal(np_(mh.ell.indices), hi) and np_(mh.ell.data).tobytes() == hd.tobytes()
+    assert np.array_equal(np_(mh.coo_tail.row), tail[0]) and np.array_equal(np_(mh.coo_tail.col), tail[1])
+    assert np_(mh.coo_tail.data).tobytes() == tail[2].tobytes()
+    assert_within(sp.spmv("hyb", mh, x), ref, bound)
