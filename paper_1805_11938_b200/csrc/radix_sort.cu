@@ -54,12 +54,12 @@ struct RsTileSmem {
   uint32_t dstart[RS_RADIX];
   uint32_t gbase[RS_RADIX];
   uint32_t tmp[RS_THREADS / 32 + 1];
+  uint32_t thist[RS_RADIX];  // the tile's digit counts (onesweep: published before the ranking)
   uint32_t tile;
 };
 
-__device__ __forceinline__ void rs_rank_tile(RsTileSmem& sm, const uint64_t* __restrict__ keys_in, int64_t n,
-                                             int64_t tile_base, int shift, unsigned mask,
-                                             uint64_t (&key)[RS_LANE_ITEMS], uint32_t (&rank)[RS_LANE_ITEMS]) {
+__device__ __forceinline__ void rs_load_tile(const uint64_t* __restrict__ keys_in, int64_t n, int64_t tile_base,
+                                             uint64_t (&key)[RS_LANE_ITEMS]) {
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t warp_base = tile_base + static_cast<int64_t>(warp) * RS_WARP_ITEMS;
 #pragma unroll
@@ -67,6 +67,13 @@ __device__ __forceinline__ void rs_rank_tile(RsTileSmem& sm, const uint64_t* __r
     const int64_t idx = warp_base + r * 32 + lane;
     key[r] = idx < n ? keys_in[idx] : 0;
   }
+}
+
+__device__ __forceinline__ void rs_rank_loaded(RsTileSmem& sm, int64_t n, int64_t tile_base, int shift, unsigned mask,
+                                               const uint64_t (&key)[RS_LANE_ITEMS],
+                                               uint32_t (&rank)[RS_LANE_ITEMS]) {
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t warp_base = tile_base + static_cast<int64_t>(warp) * RS_WARP_ITEMS;
 #pragma unroll
   for (int r = 0; r < RS_LANE_ITEMS; ++r) {
     const int64_t idx = warp_base + r * 32 + lane;
@@ -82,6 +89,13 @@ __device__ __forceinline__ void rs_rank_tile(RsTileSmem& sm, const uint64_t* __r
     // per-warp exclusive prefixes (rs_write_tile adds dstart and wcnt)
     rank[r] = before + __popc(peers & lanemask_lt());
   }
+}
+
+__device__ __forceinline__ void rs_rank_tile(RsTileSmem& sm, const uint64_t* __restrict__ keys_in, int64_t n,
+                                             int64_t tile_base, int shift, unsigned mask,
+                                             uint64_t (&key)[RS_LANE_ITEMS], uint32_t (&rank)[RS_LANE_ITEMS]) {
+  rs_load_tile(keys_in, n, tile_base, key);
+  rs_rank_loaded(sm, n, tile_base, shift, mask, key, rank);
 }
 
 // Writes the ranked tile out: keys through shared memory in digit order
@@ -104,6 +118,14 @@ __device__ __forceinline__ void rs_write_tile(RsTileSmem& sm, int64_t n, int64_t
       sm.buf[rank[r]] = key[r];
     }
   }
+  // the values' loads are issued now (the key registers are dead) and land
+  // while the keys are written out
+  V vv[RS_LANE_ITEMS];
+#pragma unroll
+  for (int r = 0; r < RS_LANE_ITEMS; ++r) {
+    const int64_t idx = warp_base + r * 32 + lane;
+    vv[r] = idx < n ? (vals_in ? vals_in[idx] : static_cast<V>(idx)) : V(0);
+  }
   __syncthreads();
   int64_t count = n - tile_base;
   if (count > RS_TILE) count = RS_TILE;
@@ -119,7 +141,7 @@ __device__ __forceinline__ void rs_write_tile(RsTileSmem& sm, int64_t n, int64_t
 #pragma unroll
   for (int r = 0; r < RS_LANE_ITEMS; ++r) {
     const int64_t idx = warp_base + r * 32 + lane;
-    if (idx < n) vbuf[rank[r]] = vals_in ? vals_in[idx] : static_cast<V>(idx);
+    if (idx < n) vbuf[rank[r]] = vv[r];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < count; i += RS_THREADS) {
@@ -217,24 +239,34 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MIN_BLOCKS) k_rs_onesweep(const
                                                             uint32_t* __restrict__ tile_counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RsTileSmem& sm = *reinterpret_cast<RsTileSmem*>(smem_raw);
+  const int d = threadIdx.x;
   if (threadIdx.x == 0) sm.tile = atomicAdd(tile_counter, 1u);
   for (int i = threadIdx.x; i < RS_WARPS * RS_RADIX; i += RS_THREADS) (&sm.wcnt[0][0])[i] = 0;
+  sm.thist[d] = 0;
   __syncthreads();
   const int64_t t = sm.tile;
   const int64_t tile_base = t * RS_TILE;
   uint64_t key[RS_LANE_ITEMS];
   uint32_t rank[RS_LANE_ITEMS];
-  rs_rank_tile(sm, keys_in, n, tile_base, shift, mask, key, rank);
+  rs_load_tile(keys_in, n, tile_base, key);
+  // the tile's digit counts first, published at once so that successors'
+  // look-backs find them while this tile is still ranking
+  {
+    const int64_t warp_base = tile_base + static_cast<int64_t>(threadIdx.x >> 5) * RS_WARP_ITEMS + (threadIdx.x & 31);
+#pragma unroll
+    for (int r = 0; r < RS_LANE_ITEMS; ++r)
+      if (warp_base + r * 32 < n) atomicAdd(&sm.thist[rs_digit(key[r], shift, mask)], 1u);
+  }
   __syncthreads();
-  const int d = threadIdx.x;
-  const uint32_t total = rs_warp_prefix(sm);
-  // publish this tile's count, then look back for the exclusive prefix
+  const uint32_t total = sm.thist[d];
   uint32_t* mine = status + t * RS_RADIX + d;
+  st_relaxed_gpu(mine, (t == 0 ? RS_FLAG_PRE : RS_FLAG_AGG) | total);
+  rs_rank_loaded(sm, n, tile_base, shift, mask, key, rank);
+  __syncthreads();
+  rs_warp_prefix(sm);
+  // look back for the exclusive prefix
   uint32_t excl = 0;
-  if (t == 0) {
-    st_relaxed_gpu(mine, RS_FLAG_PRE | total);
-  } else {
-    st_relaxed_gpu(mine, RS_FLAG_AGG | total);
+  if (t > 0) {
     for (int64_t j = t - 1;;) {
       const uint32_t w = ld_relaxed_gpu(status + j * RS_RADIX + d);
       if ((w & ~RS_VAL_MASK) == 0) continue;  // predecessor not there yet
