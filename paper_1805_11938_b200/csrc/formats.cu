@@ -49,13 +49,14 @@ __global__ void k_csr5_scatter(int64_t k0, int64_t nnz, int64_t tile, int64_t si
   }
 }
 
-// Full tiles (tile = omega*sigma <= CSR5_SMEM_TILE entries): one tile per
-// block iteration, read in CSR order (coalesced), transposed to the stored
-// order (sigma x omega grid, row-major; formats.py:204-209) in shared memory
-// and written out coalesced.  32-bit in-tile arithmetic.
+// Full tiles (tile = omega*sigma <= CSR5_SMEM_TILE entries): `group`
+// consecutive tiles (contiguous in memory) per block iteration, read in CSR
+// order (coalesced), transposed to the stored order (sigma x omega grid,
+// row-major; formats.py:204-209) in shared memory and written out
+// coalesced.  32-bit in-tile arithmetic.
 constexpr int CSR5_SMEM_TILE = 4096;
-__global__ void __launch_bounds__(256) k_csr5_scatter_tiles(int64_t full_tiles, int tile, int omega, int sigma,
-                                                            const uint8_t* __restrict__ flags_csr,
+__global__ void __launch_bounds__(256) k_csr5_scatter_tiles(int64_t full_tiles, int tile, int group, int omega,
+                                                            int sigma, const uint8_t* __restrict__ flags_csr,
                                                             const int32_t* __restrict__ col,
                                                             const double* __restrict__ val,
                                                             uint8_t* __restrict__ bit_flag,
@@ -64,26 +65,31 @@ __global__ void __launch_bounds__(256) k_csr5_scatter_tiles(int64_t full_tiles, 
   // stored slot st lives at st + st/32 (one pad word per 32: the transposed
   // writes of a warp then fall in distinct banks)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int padded = tile + tile / 32 + 1;
+  const int chunk = tile * group;
+  const int padded = chunk + chunk / 32 + 1;
   double* sv = reinterpret_cast<double*>(smem_raw);
   int32_t* sc = reinterpret_cast<int32_t*>(sv + padded);
   uint8_t* sf = reinterpret_cast<uint8_t*>(sc + padded);
-  for (int64_t t = blockIdx.x; t < full_tiles; t += gridDim.x) {
-    const int64_t base = t * tile;
-    for (int p = threadIdx.x; p < tile; p += blockDim.x) {
+  const int64_t chunks = (full_tiles + group - 1) / group;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    const int64_t base = ch * chunk;
+    const int64_t tiles_here = full_tiles - ch * group < group ? full_tiles - ch * group : group;
+    const int m = static_cast<int>(tiles_here) * tile;
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      const int tl = group > 1 ? q / tile : 0, p = q - tl * tile;
       const int gi = p % sigma, gj = p / sigma;
-      const int st = gi * omega + gj;
+      const int st = tl * tile + gi * omega + gj;
       const int sp = st + (st >> 5);
-      sv[sp] = val[base + p];
-      sc[sp] = col[base + p];
-      sf[sp] = (p == 0 || flags_csr[base + p]) ? 1 : 0;
+      sv[sp] = val[base + q];
+      sc[sp] = col[base + q];
+      sf[sp] = (p == 0 || flags_csr[base + q]) ? 1 : 0;
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < tile; p += blockDim.x) {
-      const int sp = p + (p >> 5);
-      val_out[base + p] = sv[sp];
-      col_out[base + p] = sc[sp];
-      bit_flag[base + p] = sf[sp];
+    for (int q = threadIdx.x; q < m; q += blockDim.x) {
+      const int sp = q + (q >> 5);
+      val_out[base + q] = sv[sp];
+      col_out[base + q] = sc[sp];
+      bit_flag[base + q] = sf[sp];
     }
     __syncthreads();
   }
@@ -453,11 +459,14 @@ void csr5_build(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* 
   int64_t scatter_from = 0;  // entries before this went through the shared-memory transpose
   if (tile <= CSR5_SMEM_TILE && nnz / tile > 0) {
     const int64_t full = nnz / tile;
-    const size_t smem = static_cast<size_t>(tile + tile / 32 + 1) * (sizeof(double) + sizeof(int32_t) + 1);
+    // small tiles (the reference default omega = 4: 64 entries) go several
+    // to a block iteration, ~512 entries each
+    const int group = tile >= 512 ? 1 : static_cast<int>(512 / tile);
+    const int64_t chunk = tile * group;
+    const size_t smem = static_cast<size_t>(chunk + chunk / 32 + 1) * (sizeof(double) + sizeof(int32_t) + 1);
     SPMVB_CUDA(cudaFuncSetAttribute(k_csr5_scatter_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_csr5_scatter_tiles<<<grid_for(full, 1, 148 * 8), 256, smem, s>>>(full, static_cast<int>(tile), omega, sigma,
-                                                                        flags.get(), col, val, bit_flag, col_out,
-                                                                        val_out);
+    k_csr5_scatter_tiles<<<grid_for((full + group - 1) / group, 1, 148 * 8), 256, smem, s>>>(
+        full, static_cast<int>(tile), group, omega, sigma, flags.get(), col, val, bit_flag, col_out, val_out);
     SPMVB_LAUNCHED("k_csr5_scatter_tiles");
     scatter_from = full * tile;
   }

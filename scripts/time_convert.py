@@ -17,7 +17,7 @@ from scripts.profile_kernel import PARAMS, build  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workloads", default="C4,C5")
-ap.add_argument("--formats", default="csr5")
+ap.add_argument("--formats", default="csr5")  # csr5_default: omega=4, sigma=16
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 tag = Path(os.environ.get("SPMVB_LIB_PATH", "working-tree")).name
@@ -28,7 +28,8 @@ for w in a.workloads.split(","):
         for _ in range(a.reps + 1):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            m = sp.convert(f, csr, **PARAMS[f])
+            name, kw = (f, PARAMS[f]) if f in PARAMS else ("csr5", dict(omega=4, sigma=16))
+            m = sp.convert(name, csr, **kw)
             torch.cuda.synchronize()
             ts.append((time.perf_counter() - t0) * 1e3)
             del m
