@@ -144,6 +144,54 @@ __global__ void __launch_bounds__(256) k_csr5_warp(Csr5Ctx C, int64_t t_begin, i
   if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
 }
 
+// The tile's segmented sums once the products v[] and the lane's flag mask
+// are in registers: segment ordinals by a shuffle scan of the flag counts,
+// in-lane segment sums emitted as they close, the heads of the lanes joined
+// by a segmented suffix scan (shared by the tile kernels below).
+template <int W, int S>
+__device__ __forceinline__ void csr5_tile_sums(const Csr5Ctx& C, int64_t t, int j, bool active, uint32_t fmask,
+                                               const double (&v)[S], double sc) {
+  const uint32_t aux = active ? C.aux[t] : 0u;
+  const int nflags = __popc(fmask);
+  int incl = nflags;
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    int o = __shfl_up_sync(0xffffffffu, incl, d, W);
+    if (j >= d) incl += o;
+  }
+  const int seg_base = incl - nflags;
+  double head = 0.0, sum = 0.0;
+  int seen = 0;
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      if ((fmask >> i) & 1u) {
+        if (seen == 0) head = sum;
+        else csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum);
+        ++seen;
+        sum = 0.0;
+      }
+      sum += v[i];
+    }
+  }
+  const bool F = seen > 0;
+  if (!F) head = sum;
+  double rv = head;
+  bool stop = F;
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    double ov = __shfl_down_sync(0xffffffffu, rv, d, W);
+    bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d, W) != 0;
+    if (!stop && j + d < W) {
+      rv += ov;
+      stop = ostop;
+    }
+  }
+  double right = __shfl_down_sync(0xffffffffu, rv, 1, W);
+  if (j == W - 1) right = 0.0;
+  if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
+}
+
 // Same algorithm with a compile-time sigma: each lane issues its S flag,
 // column and value loads back to back, then S independent x gathers, so a
 // warp keeps 32*S gathers in flight (random-column matrices are bound by the
@@ -270,46 +318,7 @@ __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C,
       v[i] = ok ? v[i] * ldx(C.x, cidx[i]) : 0.0;
     }
   }
-  const double sc = load_scale(C.scale_p);
-  const uint32_t aux = active ? C.aux[t] : 0u;
-  const int nflags = __popc(fmask);
-  int incl = nflags;
-#pragma unroll
-  for (int d = 1; d < W; d <<= 1) {
-    int o = __shfl_up_sync(0xffffffffu, incl, d, W);
-    if (j >= d) incl += o;
-  }
-  const int seg_base = incl - nflags;
-  double head = 0.0, sum = 0.0;
-  int seen = 0;
-  if (active) {
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-      if ((fmask >> i) & 1u) {
-        if (seen == 0) head = sum;
-        else csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum);
-        ++seen;
-        sum = 0.0;
-      }
-      sum += v[i];
-    }
-  }
-  const bool F = seen > 0;
-  if (!F) head = sum;
-  double rv = head;
-  bool stop = F;
-#pragma unroll
-  for (int d = 1; d < W; d <<= 1) {
-    double ov = __shfl_down_sync(0xffffffffu, rv, d, W);
-    bool ostop = __shfl_down_sync(0xffffffffu, stop ? 1 : 0, d, W) != 0;
-    if (!stop && j + d < W) {
-      rv += ov;
-      stop = ostop;
-    }
-  }
-  double right = __shfl_down_sync(0xffffffffu, rv, 1, W);
-  if (j == W - 1) right = 0.0;
-  if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
+  csr5_tile_sums<W, S>(C, t, j, active, fmask, v, load_scale(C.scale_p));
   zero_empty_rows();
 }
 
