@@ -138,7 +138,9 @@ extern "C" int spmvb_csr_features(int64_t n_rows, int64_t n_cols, int64_t nnz, c
     SqDev at{ptr, mean};
     k_pw_subtrees<<<grid_for(1ll << L, 128), 128, 0, s>>>(n_rows, L, at, sub.get());
     SPMVB_LAUNCHED("k_pw_subtrees");
-    k_pw_combine<<<1, 1024, (1ll << L) * sizeof(double), s>>>(n_rows, L, sub.get(), total.get());
+    const size_t smem = (1ll << L) * sizeof(double);  // up to 64 KB: above the default 48 KB
+    SPMVB_CUDA(cudaFuncSetAttribute(k_pw_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pw_combine<<<1, 1024, smem, s>>>(n_rows, L, sub.get(), total.get());
     SPMVB_LAUNCHED("k_pw_combine");
     double sumsq = 0.0;
     copy_to_host(&sumsq, total.get(), 1, s);

@@ -370,3 +370,18 @@ def test_wide_rows_sell_hyb(sp, rng):
     assert np.array_equal(np_(mh.coo_tail.row), tail[0]) and np.array_equal(np_(mh.coo_tail.col), tail[1])
     assert np_(mh.coo_tail.data).tobytes() == tail[2].tobytes()
     assert_within(sp.spmv("hyb", mh, x), ref, bound)
+
+
+@pytest.mark.parametrize("n_rows", [(1 << 24) + 5, (1 << 25) + 3, (1 << 26) + 11])
+def test_features_many_rows(sp, rng, n_rows):
+    """Row counts past 2^24 (the depth-13 pairwise combine needs 64 KB of
+    shared memory): all 8 features bit-identical to numpy."""
+    nnz = 2_000_000
+    rr = np.sort(rng.integers(0, n_rows, nnz))
+    cc = rng.integers(0, 1000, nnz)
+    a = sp.canonicalize(torch.from_numpy(rr).int().cuda(), torch.from_numpy(cc).int().cuda(),
+                        torch.ones(nnz, dtype=torch.float64, device="cuda"), n_rows, 1000)
+    r, c, v = port.canonicalize(rr, cc, np.ones(nnz), n_rows, 1000)
+    got = sp.extract_features(a).as_array()
+    want = np.array(port.extract_features(r, n_rows, 1000), dtype=np.float64)
+    assert got.tobytes() == want.tobytes(), (got, want)
