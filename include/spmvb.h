@@ -168,10 +168,17 @@ int spmvb_csr5_unstore(int64_t nnz, int omega, int sigma, const int32_t* col, co
  * slots per row; outputs sized sum(row_nnz). */
 int spmvb_ell_to_coo(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const int64_t* row_nnz,
                      int32_t* rows_out, int32_t* cols_out, double* vals_out, void* stream);
-/* SELL slices -> triplets in permuted-row order (not canonical). */
+/* SELL slices -> triplets in canonical (row, col) order. */
 int spmvb_sell_to_coo(int64_t n_rows, int64_t c, const int32_t* perm, const int64_t* slice_off,
                       const int64_t* row_nnz_perm, const int32_t* idx, const double* val, int32_t* rows_out,
                       int32_t* cols_out, double* vals_out, void* stream);
+
+/* HYB (ELL part + COO tail with its per-row offsets tail_ptr[n_rows+1]) ->
+ * triplets in canonical (row, col) order (formats.py:446-453 to_coo(hyb)). */
+int spmvb_hyb_to_coo(int64_t n_rows, int64_t k, const int32_t* ell_idx, const double* ell_val,
+                     const int64_t* ell_row_nnz, int64_t tail_nnz, const int32_t* tail_row, const int32_t* tail_col,
+                     const double* tail_val, const int32_t* tail_ptr, int32_t* rows_out, int32_t* cols_out,
+                     double* vals_out, void* stream);
 
 /* ======================================================================== */
 /* SpMV kernels — replaces kernels.py (y = scale * A x).                    */

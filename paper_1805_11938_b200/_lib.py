@@ -68,6 +68,7 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_csr5_unstore": (c_int, [c_i64, c_int, c_int, vp, vp, vp, vp, vp]),
     "spmvb_ell_to_coo": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_sell_to_coo": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvb_hyb_to_coo": (c_int, [c_i64, c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_hyb_plan": (c_int, [c_i64, vp, c_i64, c_i64, vp, P_i64, vp]),
     "spmvb_hyb_fill": (c_int, [c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_csr_chunk_size": (c_i64, []),

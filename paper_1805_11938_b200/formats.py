@@ -585,12 +585,21 @@ def to_coo(m) -> CooMatrix:
                 )
         return canonicalize(r, c, v, m.n_rows, m.n_cols, device=dev)
     if isinstance(m, HybMatrix):
-        r, c, v = _ell_triplets(m.ell)
+        # ELL part and tail merged per row on the device: already canonical
+        dev = m.device
         t = m.coo_tail
-        return canonicalize(
-            torch.cat([r, t.row]), torch.cat([c, t.col]), torch.cat([v, t.data]), m.n_rows, m.n_cols,
-            device=m.device,
-        )
+        total = m.nnz
+        r, c, v = _i32(total, dev), _i32(total, dev), _f64(total, dev)
+        if m.n_rows:
+            with torch.cuda.device(dev):
+                check(
+                    LIB.spmvb_hyb_to_coo(
+                        m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), ptr(m.ell.row_nnz), t.nnz,
+                        ptr(t.row), ptr(t.col), ptr(t.data), ptr(m.tail_ptr), ptr(r), ptr(c), ptr(v),
+                        _lib.stream(dev),
+                    )
+                )
+        return canonicalize(r, c, v, m.n_rows, m.n_cols, device=dev)
     raise TypeError(f"not a format matrix: {type(m).__name__}")
 
 

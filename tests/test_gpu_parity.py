@@ -364,12 +364,15 @@ def test_wide_rows_sell_hyb(sp, rng):
         assert np.array_equal(np_(ms.flat_indices), so.flat_indices), (c_, s_)
         assert np_(ms.flat_data).tobytes() == so.flat_data.tobytes(), (c_, s_)
         assert_within(sp.spmv("sell", ms, x), ref, bound)
+        assert sp.coo_equal(sp.to_coo(ms), a), (c_, s_)
     K, hi, hd, hn, tail = port.to_hyb(orow, ocol, oval, n)
     mh = sp.to_hyb(a)
     assert mh.k == K and np.array_equal(np_(mh.ell.indices), hi) and np_(mh.ell.data).tobytes() == hd.tobytes()
     assert np.array_equal(np_(mh.coo_tail.row), tail[0]) and np.array_equal(np_(mh.coo_tail.col), tail[1])
     assert np_(mh.coo_tail.data).tobytes() == tail[2].tobytes()
     assert_within(sp.spmv("hyb", mh, x), ref, bound)
+    assert sp.coo_equal(sp.to_coo(mh), a)
+    assert sp.coo_equal(sp.to_coo(sp.to_csr(a)), a) and sp.coo_equal(sp.to_coo(sp.to_csr5(a, 32, 16)), a)
 
 
 @pytest.mark.parametrize("n_rows", [(1 << 24) + 5, (1 << 25) + 3, (1 << 26) + 11])
