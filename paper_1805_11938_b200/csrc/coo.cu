@@ -194,14 +194,56 @@ __global__ void k_counts_to_i64(const unsigned int* __restrict__ c, int64_t n, i
     out[i] = static_cast<int64_t>(c[i]);
 }
 
+// The reference's oracle order (coo.py:128-141): y_r = ((0 + p_0) + p_1) + ...
+// with separately rounded products.  Thread per row; rows longer than
+// SEQ_LONG are left to k_spmv_sequential_long.
+constexpr int32_t SEQ_LONG = 48;
 __global__ void k_spmv_sequential(int64_t n_rows, const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
                                   const double* __restrict__ val, const double* __restrict__ x,
                                   double* __restrict__ y) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t a = ptr[r], b = ptr[r + 1];
+    if (b - a > SEQ_LONG) continue;
     double acc = 0.0;
-    for (int k = ptr[r]; k < ptr[r + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(val[k], x[col[k]]));
+    for (int k = a; k < b; ++k) acc = __dadd_rn(acc, __dmul_rn(val[k], x[col[k]]));
     y[r] = acc;
+  }
+}
+
+// One warp per long row: the lanes form 32 products at a time (the next
+// 32 already in flight), then every lane adds them in order -- the same
+// sequential recurrence, without one thread walking ~4e5 dependent loads.
+__global__ void k_spmv_sequential_long(const int32_t* __restrict__ list, int64_t n_long,
+                                       const int32_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                                       const double* __restrict__ val, const double* __restrict__ x,
+                                       double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < n_long; i += nwarps) {
+    const int32_t r = list[i];
+    const int64_t a = ptr[r], b = ptr[r + 1];
+    auto prod = [&](int64_t k) { return k < b ? __dmul_rn(val[k], x[col[k]]) : 0.0; };
+    double acc = 0.0;
+    // products of the next DEPTH chunks in flight while a chunk is summed
+    constexpr int DEPTH = 4;
+    double ring[DEPTH];
+#pragma unroll
+    for (int u = 0; u < DEPTH; ++u) ring[u] = prod(a + 32 * u + lane);
+    for (int64_t k0 = a; k0 < b; k0 += 32) {
+      const double p = ring[0];
+#pragma unroll
+      for (int u = 0; u + 1 < DEPTH; ++u) ring[u] = ring[u + 1];
+      ring[DEPTH - 1] = prod(k0 + 32 * DEPTH + lane);
+      const int m = b - k0 < 32 ? static_cast<int>(b - k0) : 32;
+      double q[32];  // all 32 broadcasts issued before the dependent adds
+#pragma unroll
+      for (int t = 0; t < 32; ++t) q[t] = __shfl_sync(0xffffffffu, p, t);
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (t < m) acc = __dadd_rn(acc, q[t]);
+    }
+    if (lane == 0) y[r] = acc;
   }
 }
 
@@ -434,6 +476,21 @@ extern "C" int spmvb_spmv_sequential(int64_t n_rows, const int32_t* ptr, const i
     if (n_rows <= 0) return;
     k_spmv_sequential<<<grid_for(n_rows, 128, 148 * 64), 128, 0, s>>>(n_rows, ptr, col, val, x, y);
     SPMVB_LAUNCHED("k_spmv_sequential");
+    DevBuf<int32_t> list(n_rows, s), total(1, s);
+    int32_t* lp = list.get();
+    exclusive_scan<int32_t>(
+        n_rows, [=] __device__(int64_t i) { return ptr[i + 1] - ptr[i] > SEQ_LONG ? 1 : 0; },
+        [=] __device__(int64_t i, int32_t v) {
+          if (ptr[i + 1] - ptr[i] > SEQ_LONG) lp[v] = static_cast<int32_t>(i);
+        },
+        OpSum{}, 0, total.get(), s);
+    int32_t n_long = 0;
+    copy_to_host(&n_long, total.get(), 1, s);
+    if (n_long > 0) {
+      k_spmv_sequential_long<<<grid_for(static_cast<int64_t>(n_long) * 32, 256, 148 * 8), 256, 0, s>>>(
+          lp, n_long, ptr, col, val, x, y);
+      SPMVB_LAUNCHED("k_spmv_sequential_long");
+    }
   });
 }
 
