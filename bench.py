@@ -304,11 +304,21 @@ def run_ours(args):
             a, b, t0, t1 = plan[k]
             sp.spmv_csr5_tiles(m, xv, out, t0, t1, a, b, scale=scale, carry=carry)
 
+    # p2p exchange with CSR5 omega=32 shards: the SpMV kernel itself stores
+    # each block's rows into the peers' next iterate (one fused kernel)
+    push_fn = None
+    if tag == "csr5" and m.omega == 32 and m.sigma in (8, 16) and not args.p2p_unfused:
+        carry_p = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=dev)
+
+        def push_fn(xv, out, scale, peers, off):
+            sp.spmv_csr5_push(m, xv, out, peers, off, scale=scale, carry=carry_p)
+
     def make_pi(exchange):
         return spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_full, exchange=exchange,
                                      local_cols=shard.indices if exchange == "sparse" else None,
                                      local_ranges=ranges if exchange in ("allgatherv", "p2p") else None,
-                                     local_spmv_range=range_fn)
+                                     local_spmv_range=range_fn,
+                                     local_spmv_push=push_fn if exchange == "p2p" else None)
 
     pi = make_pi(args.exchange)
     for _ in range(warmup):
@@ -465,6 +475,8 @@ def main():
     ap.add_argument("--exchange", choices=["allgatherv", "sparse", "p2p"], default="allgatherv",
                     help="x exchange between row blocks (N > 1): the north-star all-gather of x (default), or "
                          "only the entries each shard reads; the other one is timed too and reported")
+    ap.add_argument("--p2p-unfused", action="store_true",
+                    help="p2p exchange with a separate push kernel per row range instead of the fused SpMV+push")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)
     ap.add_argument("--cpu-keep-mod", type=int, default=64)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)

@@ -214,6 +214,18 @@ int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const doub
  * non-empty. carry: num_tiles scratch doubles.  flag_bits (may be NULL) is
  * bit_flag packed one bit per entry (spmvb_csr5_pack_flags): the tile kernel
  * then reads 64 bytes of flags per 512-entry tile instead of 512. */
+/* CSR5 SpMV fused with the multi-GPU exchange: as
+ * spmvb_spmv_csr5, and every row r of y is also stored at
+ * peers[p][push_off + r] for p < n_peers (device array of peer buffer
+ * addresses, e.g. symmetric memory mapped over NVLink): each block stores its
+ * own rows (16-byte stores) right after computing them, the carry fix-up
+ * re-stores the rows it completes.  omega = 32, sigma = 16 or 8.  The caller
+ * orders the peers' reads of those buffers (one barrier per step). */
+int spmvb_spmv_csr5_push(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                         const int32_t* tile_ptr, const uint8_t* bit_flag, const uint32_t* flag_bits,
+                         const int32_t* col, const double* val, const uint32_t* tile_aux, const int32_t* nonempty_rows,
+                         int64_t n_nonempty, double* carry, const double* x, double* y, const double* scale,
+                         const uint64_t* peers, int n_peers, int64_t push_off, void* stream);
 int spmvb_csr5_pack_flags(int64_t nnz, const uint8_t* bit_flag, uint32_t* flag_bits, void* stream);
 int spmvb_spmv_csr5(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma, const int32_t* tile_ptr,
                     const uint8_t* bit_flag, const uint32_t* flag_bits, const int32_t* col, const double* val,

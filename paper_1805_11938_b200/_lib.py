@@ -84,6 +84,10 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp],
     ),
+    "spmvb_spmv_csr5_push": (
+        c_int,
+        [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, c_int, c_i64, vp],
+    ),
     "spmvb_csr5_range_bounds": (c_int, [c_i64, c_int, c_int, vp, vp, c_int, vp, vp, vp]),
     "spmvb_spmv_csr5_tiles": (
         c_int,
@@ -135,6 +139,8 @@ def load() -> ctypes.CDLL:
                 )
             lib = ctypes.CDLL(str(_LIB_PATH))
             for name, (res, args) in SIGNATURES.items():
+                if os.environ.get("SPMVB_LIB_PATH") and not hasattr(lib, name):
+                    continue  # an older build under A/B: entry points it lacks stay unbound
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -38,6 +38,14 @@ struct Csr5Ctx {
   const double* scale_p;
 };
 
+// Fused exchange (PUSH kernels): every finished row r of y is also stored at
+// peers[p][push_off + r] (peer buffers mapped over NVLink).
+struct Csr5Push {
+  const uint64_t* peers = nullptr;
+  int n_peers = 0;
+  int64_t push_off = 0;
+};
+
 __device__ __forceinline__ int64_t csr5_row_of(const Csr5Ctx& C, int64_t g) {
   return C.nonempty ? static_cast<int64_t>(C.nonempty[g]) : g;
 }
@@ -51,6 +59,7 @@ __device__ __forceinline__ void csr5_emit(const Csr5Ctx& C, double sc, int64_t t
   const int64_t g = static_cast<int64_t>(aux & 0x7fffffffu) + s;
   C.y[csr5_row_of(C, g)] = sc * v;
 }
+
 
 // Empty rows never receive a segment: one coalesced pass writes their zeros.
 __global__ void k_csr5_empty_rows(int64_t n_rows, const int32_t* __restrict__ ptr, double* __restrict__ y) {
@@ -192,6 +201,44 @@ __device__ __forceinline__ void csr5_tile_sums(const Csr5Ctx& C, int64_t t, int 
   if (active && F) csr5_emit(C, sc, t, aux, seg_base + seen - 1, sum + right);
 }
 
+// Fused exchange epilogue of a PUSH tile kernel: the block owns the rows
+// [B(t0), B(t1)) of its tiles [t0, t1), B(t) = tile_ptr[t] (row_begin /
+// row_end at the range ends).  Once all its warps have emitted, it zeroes the
+// empty ones and stores every one of them into each peer buffer with 16-byte
+// stores (contiguous per block: a per-emit 8-byte store to the peers was
+// 2.4x costlier at C5).  A row that continues across a tile boundary is
+// stored here with its partial (or not yet written) value and again, final,
+// by the fix-up (k_csr5_fixup<true>), which runs after this grid completes.
+template <int W>
+__device__ __forceinline__ void csr5_push_block(const Csr5Ctx& C, const Csr5Push& P, int64_t t_begin, int64_t t_end,
+                                                int64_t row_begin, int64_t row_end) {
+  __syncthreads();  // the block's emits are done
+  constexpr int64_t TPB = 256 / W;
+  const int64_t t0 = t_begin + blockIdx.x * TPB;
+  const int64_t t1 = t0 + TPB < t_end ? t0 + TPB : t_end;
+  const int64_t r0 = t0 <= t_begin ? row_begin : static_cast<int64_t>(C.tile_ptr[t0]);
+  const int64_t r1 = t1 >= t_end ? row_end : static_cast<int64_t>(C.tile_ptr[t1]);
+  if (C.nonempty)
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
+      if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
+  __syncthreads();
+  const int64_t off = P.push_off;
+  // pairs (r, r+1) with off + r even: 16-byte aligned in the peer buffers
+  const int64_t first = ((off + r0) & 1) ? r0 + 1 : r0;
+  if (first > r0 && threadIdx.x == 0 && r0 < r1)
+    for (int p = 0; p < P.n_peers; ++p) reinterpret_cast<double*>(P.peers[p])[off + r0] = C.y[r0];
+  const int64_t pairs = r1 > first ? (r1 - first) / 2 : 0;
+  for (int64_t i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const int64_t r = first + 2 * i;
+    const double a = C.y[r], b = C.y[r + 1];
+    for (int p = 0; p < P.n_peers; ++p)
+      *reinterpret_cast<double2*>(reinterpret_cast<double*>(P.peers[p]) + off + r) = make_double2(a, b);
+  }
+  const int64_t last = first + 2 * pairs;
+  if (last < r1 && last >= r0 && threadIdx.x == 0)
+    for (int p = 0; p < P.n_peers; ++p) reinterpret_cast<double*>(P.peers[p])[off + last] = C.y[last];
+}
+
 // Same algorithm with a compile-time sigma: each lane issues its S flag,
 // column and value loads back to back, then S independent x gathers, so a
 // warp keeps 32*S gathers in flight (random-column matrices are bound by the
@@ -201,9 +248,9 @@ __device__ __forceinline__ void csr5_tile_sums(const Csr5Ctx& C, int64_t t, int 
 // of the empty rows of [row_begin, row_end) (a coalesced slice of ptr/y per
 // block), so that streaming pass rides along with the gather-bound tiles
 // instead of costing its own launch.
-template <int W, int S, bool EMPTIES>
-__global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
-                                                     int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
+template <int W, int S, bool EMPTIES, bool PUSH>
+__device__ __forceinline__ void csr5_tiles(const Csr5Ctx& C, const Csr5Push& P, int64_t t_begin, int64_t t_end,
+                                           int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
   const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
@@ -235,14 +282,15 @@ __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C,
         if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
     }
   };
+  auto zero_row = [&](int64_t r) { C.y[r] = 0.0; };
   auto zero_empty_rows = [&] {
     if (EMPTIES && rows_per_block > 0) {
       int64_t r = zr0 + threadIdx.x;
 #pragma unroll
       for (int k = 0; k < ZP; ++k, r += 256)
-        if (r < zr1 && zp0[k] == zp1[k]) C.y[r] = 0.0;
+        if (r < zr1 && zp0[k] == zp1[k]) zero_row(r);
       for (; r < zr1; r += blockDim.x)
-        if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
+        if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) zero_row(r);
     }
   };
   const bool active = group < t_end;
@@ -320,14 +368,31 @@ __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C,
   }
   csr5_tile_sums<W, S>(C, t, j, active, fmask, v, load_scale(C.scale_p));
   zero_empty_rows();
+  if constexpr (PUSH) csr5_push_block<W>(C, P, t_begin, t_end, row_begin, row_end);
+}
+
+template <int W, int S, bool EMPTIES>
+__global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
+                                                     int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
+  csr5_tiles<W, S, EMPTIES, false>(C, Csr5Push{}, t_begin, t_end, rows_per_block, row_begin, row_end);
+}
+
+// The same tiles fused with the exchange (csr5_push_block epilogue).
+template <int W, int S>
+__global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s_push(Csr5Ctx C, Csr5Push P, int64_t t_begin,
+                                                                          int64_t t_end, int64_t row_begin,
+                                                                          int64_t row_end) {
+  csr5_tiles<W, S, false, true>(C, P, t_begin, t_end, 0, row_begin, row_end);
 }
 
 // Carry fix-up of the continuation chains (consecutive tiles whose head
 // continues the same row) inside [t_begin, t_end), chain by chain in tile
 // order (fold_chains); the carries are already scaled.
+template <bool PUSH = false>
 __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __restrict__ tile_ptr,
                              const uint32_t* __restrict__ aux, const double* __restrict__ carry,
-                             double* __restrict__ y) {
+                             double* __restrict__ y, const uint64_t* __restrict__ peers, int n_peers,
+                             int64_t push_off) {
   pdl_wait();  // launched as a programmatic dependent of the tile kernel
   // chain key = the continued row, tile_ptr[t] (coalesced, loaded alongside
   // aux[t] rather than after it)
@@ -338,7 +403,13 @@ __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __re
         const int32_t r = tile_ptr[t];
         return (a & 0x80000000u) ? r : -1;
       },
-      [&](int64_t t) { return carry[t]; }, [&](int32_t r, double acc) { y[r] = y[r] + acc; });
+      [&](int64_t t) { return carry[t]; },
+      [&](int32_t r, double acc) {
+        const double v = y[r] + acc;
+        y[r] = v;
+        if constexpr (PUSH)
+          for (int p = 0; p < n_peers; ++p) reinterpret_cast<double*>(peers[p])[push_off + r] = v;
+      });
 }
 
 // One range of tiles, [t_begin, t_end), with the empty rows of [row_begin,
@@ -346,7 +417,7 @@ __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __re
 // inside the range.  Ranges that start at row-start tiles (the range plan)
 // fold exactly like the whole matrix, in any order.
 void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_begin, int64_t row_end,
-                  cudaStream_t s) {
+                  cudaStream_t s, const Csr5Push& P = Csr5Push{}) {
   const bool empties = C.nonempty && row_end > row_begin;
   auto empty_pass = [&] {
     if (empties) {
@@ -381,7 +452,15 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
     generic_begin = t_end;
   };
   const int omega = C.omega, sigma = C.sigma;
-  if ((sigma == 16 || sigma == 8) && (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
+  if (P.n_peers > 0) {  // fused exchange: each block also stores its rows into the peers
+    if (omega != 32 || (sigma != 16 && sigma != 8))
+      fail(SPMVB_INVALID_ARG, "the fused exchange needs omega = 32 and sigma = 16 or 8, got %d, %d", omega, sigma);
+    const int64_t blocks = ((t_end - t_begin) * 32 + 255) / 256;
+    auto kern = sigma == 16 ? k_csr5_warp_s_push<32, 16> : k_csr5_warp_s_push<32, 8>;
+    launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, C, P, t_begin, t_end, row_begin, row_end);
+    SPMVB_LAUNCHED("k_csr5_warp_s_push");
+    generic_begin = t_end;
+  } else if ((sigma == 16 || sigma == 8) && (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
     if (sigma == 16) {
       switch (omega) {
         case 32: warp_s_launch(k_csr5_warp_s<32, 16, true>, k_csr5_warp_s<32, 16, false>, 32); break;
@@ -414,8 +493,12 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
   }
   if (t_end - t_begin > 1 || t_begin > 0) {
     // one 32-tile window per warp: every window's loads are in flight at once
-    launch_pdl(k_csr5_fixup, dim3(grid_for(t_end - t_begin, 256)), dim3(256), 0, s, t_begin, t_end, C.tile_ptr,
-               C.aux, C.carry, C.y);
+    if (P.n_peers > 0)
+      launch_pdl(k_csr5_fixup<true>, dim3(grid_for(t_end - t_begin, 256)), dim3(256), 0, s, t_begin, t_end,
+                 C.tile_ptr, C.aux, C.carry, C.y, P.peers, P.n_peers, P.push_off);
+    else
+      launch_pdl(k_csr5_fixup<false>, dim3(grid_for(t_end - t_begin, 256)), dim3(256), 0, s, t_begin, t_end,
+                 C.tile_ptr, C.aux, C.carry, C.y, static_cast<const uint64_t*>(nullptr), 0, int64_t(0));
     SPMVB_LAUNCHED("k_csr5_fixup");
   }
 }
@@ -605,5 +688,39 @@ extern "C" int spmvb_csr5_pack_flags(int64_t nnz, const uint8_t* bit_flag, uint3
     if (nnz <= 0) return;
     k_csr5_pack_flags<<<grid_for((nnz + 31) / 32 * 32, 256, 148 * 16), 256, 0, s>>>(nnz, bit_flag, flag_bits);
     SPMVB_LAUNCHED("k_csr5_pack_flags");
+  });
+}
+
+extern "C" int spmvb_spmv_csr5_push(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                                    const int32_t* tile_ptr, const uint8_t* bit_flag, const uint32_t* flag_bits,
+                                    const int32_t* col, const double* val, const uint32_t* tile_aux,
+                                    const int32_t* nonempty_rows, int64_t n_nonempty, double* carry, const double* x,
+                                    double* y, const double* scale, const uint64_t* peers, int n_peers,
+                                    int64_t push_off, void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (n_peers < 0 || (n_peers > 0 && !peers)) fail(SPMVB_INVALID_ARG, "peer buffer list missing");
+    if (push_off < 0) fail(SPMVB_INVALID_ARG, "negative push offset");
+    if (n_rows <= 0) return;
+    if (omega < 1 || sigma < 1) fail(SPMVB_INVALID_ARG, "omega and sigma must be >= 1");
+    if (nnz == 0 || n_peers == 0) {  // nothing to fuse with: plain SpMV, then the rows (if any peers) pushed
+      if (nnz == 0) SPMVB_CUDA(cudaMemsetAsync(y, 0, n_rows * sizeof(double), s));
+      else {
+        Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, flag_bits, col, val, tile_aux,
+                  nonempty_rows, carry, x, y, scale};
+        const int64_t tile = static_cast<int64_t>(omega) * sigma;
+        launch_range(C, 0, (nnz + tile - 1) / tile, 0, n_rows, s);
+      }
+      if (n_peers > 0)
+        if (const int st = spmvb_push_rows(y, n_rows, peers, n_peers, push_off, stream)) {
+          const std::string msg = spmvb_last_error();
+          fail(st, "%s", msg.c_str());
+        }
+      return;
+    }
+    Csr5Ctx C{n_rows, nnz, n_nonempty, omega, sigma, ptr, tile_ptr, bit_flag, flag_bits, col, val, tile_aux,
+              nonempty_rows, carry, x, y, scale};
+    const int64_t tile = static_cast<int64_t>(omega) * sigma;
+    launch_range(C, 0, (nnz + tile - 1) / tile, 0, n_rows, s, Csr5Push{peers, n_peers, push_off});
   });
 }

@@ -146,7 +146,8 @@ class PowerIteration:
 
     def __init__(self, local_spmv: Callable, bounds, rank: int, world: int, device: torch.device,
                  x0: torch.Tensor, group=None, ops=None, exchange: str = "allgatherv",
-                 local_cols: torch.Tensor | None = None, local_ranges=None, local_spmv_range: Callable | None = None):
+                 local_cols: torch.Tensor | None = None, local_ranges=None, local_spmv_range: Callable | None = None,
+                 local_spmv_push: Callable | None = None):
         if exchange not in ("allgatherv", "sparse", "p2p"):
             raise ValueError(f"unknown exchange {exchange!r}")
         self.local_spmv = local_spmv
@@ -166,6 +167,10 @@ class PowerIteration:
         self.exchange = exchange if (world > 1 or exchange == "p2p") else "allgatherv"
         self._ranges_local = local_ranges
         self.local_spmv_range = local_spmv_range
+        # exchange="p2p" with a fused kernel: local_spmv_push(x, out, scale,
+        # peers, push_off) computes the shard and stores its rows into the
+        # peers' next iterate in the same kernel (kernels.spmv_csr5_push)
+        self.local_spmv_push = local_spmv_push
         if self.exchange == "p2p":
             self._plan_p2p(x0, n)
         if self.exchange == "sparse":
@@ -336,7 +341,10 @@ class PowerIteration:
         nxt = 1 - self._cur
         out = self.x_next[self.lo : self.hi]
         main = torch.cuda.current_stream(self.device)
-        if self._ranges_local is not None and self.local_spmv_range is not None:
+        if self.local_spmv_push is not None:
+            peers = self._peer_ptrs[nxt] if self.world > 1 else self._peer_ptrs[nxt][:0]
+            self.local_spmv_push(self.x, out, self.scale, peers, self.lo)
+        elif self._ranges_local is not None and self.local_spmv_range is not None:
             for k, (a, b) in enumerate(self._ranges_local):
                 self.local_spmv_range(k, self.x, out, self.scale)
                 ev = torch.cuda.Event()

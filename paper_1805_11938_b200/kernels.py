@@ -189,6 +189,34 @@ def spmv_csr5_tiles(m: Csr5Matrix, x: torch.Tensor, out: torch.Tensor, t_begin: 
     return y
 
 
+def spmv_csr5_push(m: Csr5Matrix, x: torch.Tensor, out: torch.Tensor, peers: torch.Tensor, push_off: int, *,
+                   scale=None, carry: torch.Tensor | None = None) -> torch.Tensor:
+    """CSR5 SpMV fused with the multi-GPU exchange (spmvb_spmv_csr5_push):
+    ``out = scale * A x`` and every row r is also stored at
+    ``peers[p][push_off + r]`` (``peers``: int64 CUDA tensor of peer buffer
+    addresses, e.g. symmetric-memory buffers of the other ranks).  Each block
+    stores its rows right after computing them; the carry fix-up re-stores the
+    rows it completes.  omega = 32, sigma = 16 or 8."""
+    xd = x.reshape(-1)
+    if not xd.is_cuda or xd.dtype != torch.float64 or xd.numel() != m.n_cols:
+        raise ValueError(f"x must be a float64 CUDA tensor of length {m.n_cols}")
+    if peers.dtype != torch.int64 or not peers.is_cuda:
+        raise ValueError("peers must be an int64 CUDA tensor of buffer addresses")
+    y = _out(m, out)
+    if carry is None:
+        carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
+    with torch.cuda.device(m.device):
+        check(
+            LIB.spmvb_spmv_csr5_push(
+                m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag),
+                ptr(_packed_flags(m)), ptr(m.indices), ptr(m.data), ptr(m.tile_aux), ptr(m.nonempty_rows),
+                m.n_nonempty, ptr(carry), ptr(xd.contiguous()), ptr(y), ptr(scale) if scale is not None else None,
+                ptr(peers), int(peers.numel()), int(push_off), _lib.stream(m.device),
+            )
+        )
+    return y
+
+
 def _spmv_csr5_host(m: Csr5Matrix, x, out, scale, ranges: int):
     if isinstance(x, torch.Tensor):
         xh = x.reshape(-1)

@@ -78,14 +78,19 @@ def test_p2p_power_iteration_world1(sp, rng):
     p2p = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0, exchange="p2p")
     p2r = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0, exchange="p2p",
                                 local_ranges=[(a0, b0) for a0, b0, _, _ in plan], local_spmv_range=range_fn)
+    p2f = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0, exchange="p2p",
+                                local_spmv_push=lambda xv, out, scale, peers, off: sp.spmv_csr5_push(
+                                    m, xv, out, peers, off, scale=scale))
     assert p2p.exchange == "p2p"
     for _ in range(7):
         ref.step()
         p2p.step()
         p2r.step()
+        p2f.step()
     torch.cuda.synchronize()
     want = ref.x.cpu().numpy()
-    for pi in (p2p, p2r):
+    assert p2f.gather_full().cpu().numpy().tobytes() == p2p.gather_full().cpu().numpy().tobytes()
+    for pi in (p2p, p2r, p2f):
         got = pi.gather_full().cpu().numpy()
         np.testing.assert_allclose(got, want, rtol=1e-14, atol=0)
         assert float(pi.scale.item()) == pytest.approx(float(ref.scale.item()), rel=1e-14)
@@ -116,3 +121,42 @@ def test_power_iteration_graph_replay_identical(sp, rng):
         torch.cuda.synchronize()
         assert torch.equal(eager.x, graph.x), tag
         assert torch.equal(eager.scale, graph.scale), tag
+
+
+@pytest.mark.parametrize("sigma", [16, 8])
+@pytest.mark.parametrize("push_off", [0, 1, 1001])
+def test_fused_spmv_push_to_local_peers(sp, rng, sigma, push_off):
+    """spmvb_spmv_csr5_push: y equals the plain CSR5 SpMV bit for bit and
+    every stand-in peer buffer holds y at [push_off, push_off + n) with the
+    rest untouched -- empty rows, rows spanning several tiles and blocks,
+    and odd offsets (the 16-byte store path) included."""
+    n, nc = 30_000, 20_000
+    counts = np.where(rng.random(n) < 0.4, 0, rng.integers(1, 30, n))
+    counts[[5, 17_000, 29_999]] = [9_000, 3_000, 700]  # rows across many tiles / blocks, last row long
+    rr = np.repeat(np.arange(n), counts)
+    cc = np.concatenate([np.sort(rng.choice(nc, size=k, replace=False)) for k in counts if k])
+    vv = rng.normal(size=rr.size)
+    a = sp.canonicalize(torch.from_numpy(rr).int(), torch.from_numpy(cc).int(), vv, n, nc)
+    m = sp.to_csr5(a, 32, sigma)
+    x = torch.from_numpy(rng.normal(size=nc)).cuda()
+    scale = torch.tensor([0.75], dtype=torch.float64, device="cuda")
+    ref = sp.spmv_csr5(m, x, scale=scale)
+    peers = [torch.full((push_off + n + 3,), -7.0, dtype=torch.float64, device="cuda") for _ in range(3)]
+    ptrs = torch.tensor([p.data_ptr() for p in peers], dtype=torch.int64, device="cuda")
+    y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    sp.spmv_csr5_push(m, x, y, ptrs, push_off, scale=scale)
+    torch.cuda.synchronize()
+    assert y.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
+    for p in peers:
+        h = p.cpu().numpy()
+        assert h[push_off:push_off + n].tobytes() == y.cpu().numpy().tobytes()
+        assert np.all(h[:push_off] == -7.0) and np.all(h[push_off + n:] == -7.0)
+
+
+def test_fused_spmv_push_rejects_other_shapes(sp, rng):
+    rr = np.array([0, 1, 2]); cc = np.array([0, 1, 2]); vv = np.ones(3)
+    m = sp.to_csr5(sp.canonicalize(rr, cc, vv, 3, 3), 4, 16)
+    p = torch.zeros(3, dtype=torch.float64, device="cuda")
+    ptrs = torch.tensor([p.data_ptr()], dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError, match="omega"):
+        sp.spmv_csr5_push(m, torch.ones(3, dtype=torch.float64, device="cuda"), None, ptrs, 0)
