@@ -109,8 +109,26 @@ def dist_env():
     return world, rank, local
 
 
+# stdout carries exactly one JSON line: everything else written to file
+# descriptor 1 (e.g. NCCL's "NCCL version ..." banner under NCCL_DEBUG=VERSION,
+# printed from C at communicator creation) is redirected to stderr, and the
+# JSON line goes to the saved original stdout.
+_JSON_FD = None
+
+
+def _isolate_stdout():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
 def emit(obj):
-    print(json.dumps(obj), flush=True)
+    line = json.dumps(obj) + "\n"
+    if _JSON_FD is None:
+        print(line, end="", flush=True)
+    else:
+        os.write(_JSON_FD, line.encode())
 
 
 # --------------------------------------------------------------------------
@@ -181,6 +199,15 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif args.exchange == "p2p":
+        # the peer-memory exchange rendezvouses its symmetric buffers over a
+        # process group: a one-rank group on 127.0.0.1 for a single GPU
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
     w = WORKLOADS[args.workload]
     warmup = max(args.warmup, 3)
 
@@ -482,6 +509,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    _isolate_stdout()
     if args.impl == "reference":
         run_reference(args)
     else:
