@@ -249,7 +249,10 @@ void for_long_rows(Count count, int64_t n, F f, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_LANE_ITEMS = 16;                        // per lane
+#ifndef SPMVB_RS_LANE_ITEMS
+#define SPMVB_RS_LANE_ITEMS 16
+#endif
+constexpr int RS_LANE_ITEMS = SPMVB_RS_LANE_ITEMS;       // per lane
 constexpr int RS_WARP_ITEMS = 32 * RS_LANE_ITEMS;        // 512
 constexpr int RS_TILE = RS_WARPS * RS_WARP_ITEMS;        // 4096
 constexpr int RS_RADIX = 256;
