@@ -220,6 +220,11 @@ def run_ours(args):
     t0 = time.perf_counter()
     a = sp.canonicalize(r, c, v, n, n)
     torch.cuda.synchronize()
+    t_canon_first = time.perf_counter() - t0  # includes growing the memory pool
+    del a
+    t0 = time.perf_counter()
+    a = sp.canonicalize(r, c, v, n, n)
+    torch.cuda.synchronize()
     t_canon = time.perf_counter() - t0
     raw_nnz = int(r.numel())
     del r, c, v
@@ -472,7 +477,8 @@ def run_ours(args):
             "exchange": exchange,
             "clocks": clk,
             "formats": formats,
-            "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "to_csr_s": t_csr,
+            "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "canonicalize_first_call_s": t_canon_first,
+                           "to_csr_s": t_csr,
                            "canonicalize_Mentries_per_s": raw_nnz / t_canon / 1e6},
         })
     if world > 1:
