@@ -421,24 +421,36 @@ def run_ours(args):
             exchange["rank0_volume_entries"] = vol
 
     # ---- end to end through the public API with host buffers ----
-    # (host x in, host y out; the output buffer is the caller's, like numpy's out=)
-    x_host = x_full.cpu().pin_memory()
-    y_host = torch.empty(m.n_rows, dtype=torch.float64).pin_memory()
-    e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    sp.spmv(tag, m, x_host, out=y_host)
+    # Every step copies its x in from pinned host memory and its y back to a
+    # caller-owned pinned host buffer.  Headline: spmv_many over the steps'
+    # vectors (step k+1's x is copied in while step k computes and its y is
+    # copied back: both PCIe directions busy); also reported: one synchronous
+    # spmv(..., out=) call per step.
+    x_hosts = [x_full.cpu().pin_memory() for _ in range(2)]
+    y_hosts = [torch.empty(m.n_rows, dtype=torch.float64).pin_memory() for _ in range(2)]
+    e2e_steps = max(2, min(args.steps, args.e2e_steps))
+    sp.spmv(tag, m, x_hosts[0], out=y_hosts[0])
+    sp.spmv_many(tag, m, x_hosts, y_hosts)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        sp.spmv(tag, m, x_host, out=y_host)
+    sp.spmv_many(tag, m, [x_hosts[k % 2] for k in range(e2e_steps)], [y_hosts[k % 2] for k in range(e2e_steps)])
     t_e2e = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sp.spmv(tag, m, x_hosts[0], out=y_hosts[0])
+    t_single = time.perf_counter() - t0
     if world > 1:
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_e2e, t_single], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
+        t_e2e, t_single = float(tt[0].item()), float(tt[1].item())
     e2e = {"value": 2.0 * nnz * e2e_steps / t_e2e / 1e9, "unit": "GFLOP/s",
-           "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(y_host.numel() * 8),
-           "steps": e2e_steps, "api": f"paper_1805_11938_b200.spmv('{tag}', m, pinned_host_x, out=pinned_host_y)"}
+           "h2d_bytes_per_step": int(x_hosts[0].numel() * 8), "d2h_bytes_per_step": int(y_hosts[0].numel() * 8),
+           "steps": e2e_steps,
+           "api": f"paper_1805_11938_b200.spmv_many('{tag}', m, pinned_host_xs, pinned_host_ys) "
+                  "(transfers pipelined across the steps' vectors)",
+           "single_call_value": 2.0 * nnz * e2e_steps / t_single / 1e9,
+           "single_call_api": f"paper_1805_11938_b200.spmv('{tag}', m, pinned_host_x, out=pinned_host_y) per step"}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None

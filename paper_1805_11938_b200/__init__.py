@@ -67,7 +67,9 @@ from .harness import (  # noqa: E402
     times_by_matrix,
     write_records,
 )
-from .kernels import spmv, spmv_csr, spmv_csr5, spmv_csr5_push, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_sell  # noqa: E402
+from .kernels import (  # noqa: E402
+    spmv, spmv_csr, spmv_csr5, spmv_csr5_push, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_many, spmv_sell,
+)
 from .model import (  # noqa: E402
     DecisionTreeModel,
     ModelIOError,

@@ -25,8 +25,8 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import Csr5Matrix, CsrMatrix, EllMatrix, FormatMatrix, FormatTag, HybMatrix, SellMatrix
 
-__all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_tiles", "spmv_ell", "spmv_hyb",
-           "spmv_sell"]
+__all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push", "spmv_csr5_tiles", "spmv_ell",
+           "spmv_hyb", "spmv_many", "spmv_sell"]
 
 
 def plan_row_blocks(n_rows: int, workers: int) -> list[tuple[int, int]]:
@@ -310,3 +310,91 @@ def spmv(tag: FormatTag, m: FormatMatrix, x, workers: int = 1, **kw):
     if not isinstance(m, cls):
         raise ValueError(f"format tag {FormatTag(tag).value!r} does not match {type(m).__name__}")
     return kernel(m, x, workers, **kw)
+
+
+def spmv_many(tag: FormatTag, m: FormatMatrix, xs, outs, *, scale=None, ranges: int = 16) -> list:
+    """y_k = A x_k for a sequence of host vectors, transfers pipelined across
+    vectors.  ``xs``: pinned float64 CPU tensors of length n_cols; ``outs``:
+    pinned float64 CPU tensors of length n_rows (written in place, returned).
+
+    The same results as ``spmv(tag, m, x_k, out=y_k)`` one after the other,
+    bit for bit; but x_{k+1}'s host->device copy runs while y_k is computed
+    and copied back (the PCIe link carries both directions at once), on two
+    device buffer pairs.  CSR5 streams each of ``ranges`` row-aligned tile
+    ranges back as soon as it is finished (as the single-vector host path);
+    the other formats copy y_k back after its SpMV.  Returns ``outs``."""
+    tag = FormatTag(tag)
+    cls, _ = _KERNELS[tag]
+    if not isinstance(m, cls):
+        raise ValueError(f"format tag {tag.value!r} does not match {type(m).__name__}")
+    xs, outs = list(xs), list(outs)
+    if len(xs) != len(outs):
+        raise ValueError(f"{len(xs)} inputs but {len(outs)} outputs")
+    for xh in xs:
+        if not (isinstance(xh, torch.Tensor) and not xh.is_cuda and xh.is_pinned() and xh.dtype == torch.float64):
+            raise ValueError("spmv_many needs pinned float64 CPU tensors (torch.empty(..., pin_memory=True))")
+        if xh.numel() != m.n_cols:
+            raise ValueError(f"x has length {xh.numel()}, expected {m.n_cols}")
+    for yh in outs:
+        if not (isinstance(yh, torch.Tensor) and not yh.is_cuda and yh.is_pinned() and yh.dtype == torch.float64):
+            raise ValueError("spmv_many needs pinned float64 CPU output tensors")
+        if yh.numel() != m.n_rows or not yh.is_contiguous():
+            raise ValueError(f"out must be a contiguous tensor of length {m.n_rows}")
+    if not xs:
+        return outs
+    dev = m.device
+    with torch.cuda.device(dev):
+        comp = torch.cuda.current_stream(dev)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        s_in.wait_stream(comp)
+        s_out.wait_stream(comp)
+        xd = [torch.empty(max(m.n_cols, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        yd = [torch.empty(max(m.n_rows, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        x_free = [None, None]  # compute of the vector that last used xd[b] done
+        y_free = [None, None]  # copy-back of the vector that last used yd[b] done
+        plan = None
+        if tag is FormatTag.CSR5 and m.nnz > 0 and m.n_rows > 0:
+            tb, rb = m.range_plan(ranges)
+            k_all = len(tb) - 1
+            plan = [(int(rb[k]), int(rb[k + 1]) if k + 1 < k_all else m.n_rows, int(tb[k]), int(tb[k + 1]))
+                    for k in range(k_all)][::-1]  # light rows (last ranges) first
+            carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=dev)
+        for k, (xh, yh) in enumerate(zip(xs, outs)):
+            b = k % 2
+            with torch.cuda.stream(s_in):
+                if x_free[b] is not None:
+                    s_in.wait_event(x_free[b])
+                xd[b][: m.n_cols].copy_(xh.reshape(-1), non_blocking=True)
+                x_in = torch.cuda.Event()
+                x_in.record(s_in)
+            comp.wait_event(x_in)
+            if y_free[b] is not None:
+                comp.wait_event(y_free[b])
+            xv, yv = xd[b][: m.n_cols], yd[b][: m.n_rows]
+            yflat = yh.reshape(-1)
+            if plan is not None:
+                for a, e, t0, t1 in plan:
+                    spmv_csr5_tiles(m, xv, yv, t0, t1, a, e, scale=scale, carry=carry)
+                    if e > a:
+                        done = torch.cuda.Event()
+                        done.record(comp)
+                        s_out.wait_event(done)
+                        with torch.cuda.stream(s_out):
+                            yflat[a:e].copy_(yv[a:e], non_blocking=True)
+            else:
+                spmv(tag, m, xv, out=yv, scale=scale)
+                done = torch.cuda.Event()
+                done.record(comp)
+                s_out.wait_event(done)
+                with torch.cuda.stream(s_out):
+                    yflat.copy_(yv, non_blocking=True)
+            x_free[b] = torch.cuda.Event()
+            x_free[b].record(comp)
+            y_free[b] = torch.cuda.Event()
+            y_free[b].record(s_out)
+            # the host buffers stay referenced by the caller; the device ones
+            # are released only after the streams below are joined
+        comp.wait_stream(s_in)
+        comp.wait_stream(s_out)
+        comp.synchronize()
+    return outs

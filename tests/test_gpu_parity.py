@@ -388,3 +388,21 @@ def test_features_many_rows(sp, rng, n_rows):
     got = sp.extract_features(a).as_array()
     want = np.array(port.extract_features(r, n_rows, 1000), dtype=np.float64)
     assert got.tobytes() == want.tobytes(), (got, want)
+
+
+@pytest.mark.parametrize("tag,kw", [("csr5", dict(omega=32, sigma=16)), ("csr", {}), ("hyb", {}), ("sell", dict(sell_c=32))])
+def test_spmv_many_pipelined_matches_single_calls(sp, rng, tag, kw):
+    """spmv_many (host vectors, transfers pipelined across vectors on two
+    device buffer pairs) == spmv(..., out=) one call at a time, bit for bit."""
+    rr, cc, vv, nr, nc = random_triplets(rng, max_dim=3000)
+    a = sp.canonicalize(rr, cc, vv, nr, nc)
+    m = sp.convert(tag, a, **kw)
+    xs = [torch.from_numpy(rng.normal(size=nc)).pin_memory() for _ in range(5)]
+    ys = [torch.full((nr,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(5)]
+    out = sp.spmv_many(tag, m, xs, ys, ranges=4)
+    assert len(out) == len(ys) and all(o is y for o, y in zip(out, ys))
+    for xh, yh in zip(xs, ys):
+        want = sp.spmv(tag, m, xh.cuda()).cpu()
+        assert yh.numpy().tobytes() == want.numpy().tobytes()
+    with pytest.raises(ValueError, match="pinned"):
+        sp.spmv_many(tag, m, [xs[0].clone()], [ys[0]])
