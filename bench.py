@@ -510,7 +510,7 @@ def main():
     # default command is cheap and stable under ncu's serialised replay.
     ap.add_argument("--formats", default="csr5")
     ap.add_argument("--kernel-reps", type=int, default=20)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--overlap-ranges", type=int, default=4,
                     help="N > 1, CSR5 shards: row ranges whose all-gatherv overlaps the remaining local SpMV")
     ap.add_argument("--balance", choices=["nnz", "cost"], default="nnz",
