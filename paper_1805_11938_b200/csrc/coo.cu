@@ -20,14 +20,26 @@ struct spmvb_canon {
   uint64_t* skeys = nullptr;
   const double* svals = nullptr;
   DevBuf<uint32_t> tile_off;  // kept runs before each compaction tile
+  DevBuf<uint32_t> hist;      // radix digit counts taken by the key build
 };
 
 namespace {
 
+constexpr int CANON_HIST_COPIES = 4;  // shared-memory digit-count copies per block (warp & 3)
+constexpr int CANON_MAX_PASSES = 8;
+
 template <typename I>
 __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__ col, const double* __restrict__ val,
                                 int64_t n, int64_t n_rows, int64_t n_cols, int colbits, uint64_t* __restrict__ keys,
-                                unsigned long long* bad, int* noncanonical) {
+                                unsigned long long* bad, int* noncanonical, int passes, int key_bits,
+                                uint32_t* __restrict__ hist) {
+  // the radix sort's digit counts of every pass, taken while the keys are
+  // in registers (passes == 0: not wanted)
+  __shared__ uint32_t cnt[CANON_HIST_COPIES][CANON_MAX_PASSES * 256];
+  for (int i = threadIdx.x; i < CANON_HIST_COPIES * passes * 256; i += blockDim.x)
+    cnt[i / (passes * 256)][i % (passes * 256)] = 0;
+  __syncthreads();
+  uint32_t* mine = cnt[(threadIdx.x >> 5) & (CANON_HIST_COPIES - 1)];
   // flags are reduced per block before touching global memory: unsorted
   // input would otherwise put one atomic per entry on a single address.
   // U warp-contiguous groups per thread are loaded before any is used; the
@@ -60,7 +72,12 @@ __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__
       }
       if (i >= n) continue;
       const bool oob = r[u] < 0 || r[u] >= n_rows || c[u] < 0 || c[u] >= n_cols;
-      keys[i] = oob ? 0ull : ((static_cast<uint64_t>(r[u]) << colbits) | static_cast<uint64_t>(c[u]));
+      const uint64_t key = oob ? 0ull : ((static_cast<uint64_t>(r[u]) << colbits) | static_cast<uint64_t>(c[u]));
+      keys[i] = key;
+      for (int p = 0, sh = 0; p < passes; ++p, sh += 8) {
+        const int nb = key_bits - sh < 8 ? key_bits - sh : 8;
+        atomicAdd(&mine[p * 256 + static_cast<unsigned>((key >> sh) & ((1u << nb) - 1u))], 1u);
+      }
       if (oob) atomicMin(bad, static_cast<unsigned long long>(i));  // rare: any out-of-range entry aborts
       bool nc = (v[u] == 0.0);
       if (i > 0 && !oob && (pr[u] > r[u] || (pr[u] == r[u] && pc[u] >= c[u]))) nc = true;
@@ -68,6 +85,12 @@ __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__
     }
   }
   if (__syncthreads_or(nc_any) && threadIdx.x == 0) atomicOr(noncanonical, 1);
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int c = 0; c < CANON_HIST_COPIES; ++c) t += cnt[c][i];
+    if (t) atomicAdd(&hist[i], t);
+  }
 }
 
 // Runs of equal keys in the sorted stream; the values were carried through
@@ -289,14 +312,20 @@ extern "C" int spmvb_canonicalize_begin(const void* row, const void* col, int in
         SPMVB_CUDA(cudaMemcpyAsync(d_bad.get(), &init_bad, sizeof(init_bad), cudaMemcpyHostToDevice, s));
         SPMVB_CUDA(cudaMemcpyAsync(d_flag.get(), &init_flag, sizeof(init_flag), cudaMemcpyHostToDevice, s));
         unsigned g = grid_for(nnz_in, 256, 148 * 16);
+        // digit counts for the single-pass radix sort (below 2^30 items)
+        const int key_bits = rowbits + p->colbits;
+        const int passes = (nnz_in < (1ll << 30) && key_bits > 0) ? (key_bits + 7) / 8 : 0;
+        if (passes > CANON_MAX_PASSES) fail(SPMVB_INTERNAL, "key of %d bits", key_bits);
+        p->hist = DevBuf<uint32_t>(passes > 0 ? passes * 256 : 1, s);
+        if (passes > 0) SPMVB_CUDA(cudaMemsetAsync(p->hist.get(), 0, passes * 256 * sizeof(uint32_t), s));
         if (index_width == 4)
           k_canon_prepare<int32_t><<<g, 256, 0, s>>>(static_cast<const int32_t*>(row), static_cast<const int32_t*>(col),
                                                      val, nnz_in, n_rows, n_cols, p->colbits, p->keys_a.get(),
-                                                     d_bad.get(), d_flag.get());
+                                                     d_bad.get(), d_flag.get(), passes, key_bits, p->hist.get());
         else
           k_canon_prepare<int64_t><<<g, 256, 0, s>>>(static_cast<const int64_t*>(row), static_cast<const int64_t*>(col),
                                                      val, nnz_in, n_rows, n_cols, p->colbits, p->keys_a.get(),
-                                                     d_bad.get(), d_flag.get());
+                                                     d_bad.get(), d_flag.get(), passes, key_bits, p->hist.get());
         SPMVB_LAUNCHED("k_canon_prepare");
         unsigned long long h_bad = 0;
         int h_flag = 0;
@@ -331,7 +360,8 @@ extern "C" int spmvb_canonicalize_begin(const void* row, const void* col, int in
           uint32_t h_total = 0;
           RadixSortResult64 rs =
               radix_sort_pairs64(p->keys_a.get(), p->keys_b.get(), reinterpret_cast<const uint64_t*>(val),
-                                 p->vals_a.get(), p->vals_b.get(), nnz_in, rowbits + p->colbits, s);
+                                 p->vals_a.get(), p->vals_b.get(), nnz_in, rowbits + p->colbits, s,
+                                 passes > 0 ? p->hist.get() : nullptr);
           p->skeys = rs.keys;
           p->svals = reinterpret_cast<const double*>(rs.vals);
           const int64_t tiles = (nnz_in + CANON_TILE - 1) / CANON_TILE;

@@ -274,7 +274,11 @@ RadixSortResult radix_sort_pairs(uint64_t* keys_a, uint32_t* vals_a, uint64_t* k
 // Sorts keys_a carrying 8-byte values read from vals_in (left unmodified);
 // keys_b, vals_a and vals_b are ping-pong storage.  Returns the buffers that
 // hold the result (keys_a or keys_b; vals_a or vals_b).
+// digit_hist (optional, device): the digit counts of every pass already
+// taken by the caller while building the keys, hist[p*256 + d] for the
+// ceil(key_bits/8) passes (saves the sort its own read of the keys).
 RadixSortResult64 radix_sort_pairs64(uint64_t* keys_a, uint64_t* keys_b, const uint64_t* vals_in, uint64_t* vals_a,
-                                     uint64_t* vals_b, int64_t n, int key_bits, cudaStream_t s);
+                                     uint64_t* vals_b, int64_t n, int key_bits, cudaStream_t s,
+                                     const uint32_t* digit_hist = nullptr);
 
 }  // namespace spmvb

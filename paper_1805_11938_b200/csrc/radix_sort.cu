@@ -350,7 +350,7 @@ namespace {
 // ping-pong b <-> a.  Returns the buffers holding the result.
 template <typename V>
 std::pair<uint64_t*, V*> sort_passes(uint64_t* keys_a, uint64_t* keys_b, const V* vin, V* vals_a, V* vals_b, int64_t n,
-                                     int key_bits, cudaStream_t s) {
+                                     int key_bits, cudaStream_t s, const uint32_t* hist_in = nullptr) {
   const int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
   const int passes = (key_bits + 7) / 8;
   const size_t smem = sizeof(RsTileSmem);
@@ -372,10 +372,16 @@ std::pair<uint64_t*, V*> sort_passes(uint64_t* keys_a, uint64_t* keys_b, const V
     DevBuf<uint32_t> hist(static_cast<size_t>(passes) * RS_RADIX, s);
     DevBuf<uint32_t> status(static_cast<size_t>(tiles) * RS_RADIX, s);
     DevBuf<uint32_t> counters(passes, s);
-    SPMVB_CUDA(cudaMemsetAsync(hist.get(), 0, passes * RS_RADIX * sizeof(uint32_t), s));
     SPMVB_CUDA(cudaMemsetAsync(counters.get(), 0, passes * sizeof(uint32_t), s));
-    k_rs_hist_all<<<grid_for(n, RS_HIST_WARPS * 32, 148 * 8), RS_HIST_WARPS * 32, 0, s>>>(keys_a, n, passes, key_bits, hist.get());
-    SPMVB_LAUNCHED("k_rs_hist_all");
+    if (hist_in) {
+      SPMVB_CUDA(cudaMemcpyAsync(hist.get(), hist_in, passes * RS_RADIX * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                 s));
+    } else {
+      SPMVB_CUDA(cudaMemsetAsync(hist.get(), 0, passes * RS_RADIX * sizeof(uint32_t), s));
+      k_rs_hist_all<<<grid_for(n, RS_HIST_WARPS * 32, 148 * 8), RS_HIST_WARPS * 32, 0, s>>>(keys_a, n, passes,
+                                                                                          key_bits, hist.get());
+      SPMVB_LAUNCHED("k_rs_hist_all");
+    }
     k_rs_digit_offsets<<<passes, RS_RADIX, 0, s>>>(hist.get());
     SPMVB_LAUNCHED("k_rs_digit_offsets");
     for (int p = 0; p < passes; ++p) {
@@ -432,14 +438,15 @@ RadixSortResult radix_sort_pairs(uint64_t* keys_a, uint32_t* vals_a, uint64_t* k
 }
 
 RadixSortResult64 radix_sort_pairs64(uint64_t* keys_a, uint64_t* keys_b, const uint64_t* vals_in, uint64_t* vals_a,
-                                     uint64_t* vals_b, int64_t n, int key_bits, cudaStream_t s) {
+                                     uint64_t* vals_b, int64_t n, int key_bits, cudaStream_t s,
+                                     const uint32_t* digit_hist) {
   if (n >= (1ll << 32)) fail(SPMVB_INVALID_ARG, "radix sort supports fewer than 2^32 items");
   if (n == 0) return {keys_a, vals_a};
   if (key_bits <= 0) {
     SPMVB_CUDA(cudaMemcpyAsync(vals_a, vals_in, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     return {keys_a, vals_a};
   }
-  auto r = sort_passes<uint64_t>(keys_a, keys_b, vals_in, vals_a, vals_b, n, key_bits, s);
+  auto r = sort_passes<uint64_t>(keys_a, keys_b, vals_in, vals_a, vals_b, n, key_bits, s, digit_hist);
   return {r.first, r.second};
 }
 
