@@ -246,25 +246,42 @@ __global__ void k_spmv_sequential_long(const int32_t* __restrict__ list, int64_t
   for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; i < n_long; i += nwarps) {
     const int32_t r = list[i];
     const int64_t a = ptr[r], b = ptr[r + 1];
-    auto prod = [&](int64_t k) { return k < b ? __dmul_rn(val[k], x[col[k]]) : 0.0; };
+    // software pipeline over 32-entry chunks, D deep, slot u = chunk mod D
+    // and no register moved while its load is pending: while chunk c is
+    // summed, the x gather and value of chunk c+D (whose column index was
+    // loaded during chunk c-D) and the column index of chunk c+2D are issued
+    constexpr int D = 4;
+    int32_t rc[D];
+    double rv[D], rx[D];
+    auto ld_col = [&](int64_t k) { return k < b ? col[k] : 0; };
+#pragma unroll
+    for (int u = 0; u < D; ++u) rc[u] = ld_col(a + 32 * u + lane);  // chunks 0..D-1: columns
+#pragma unroll
+    for (int u = 0; u < D; ++u) {  // chunks 0..D-1: gathers and values; chunks D..2D-1: columns
+      const int64_t k = a + 32 * u + lane;
+      rx[u] = k < b ? x[rc[u]] : 0.0;
+      rv[u] = k < b ? val[k] : 0.0;
+      rc[u] = ld_col(k + 32 * D);
+    }
     double acc = 0.0;
-    // products of the next DEPTH chunks in flight while a chunk is summed
-    constexpr int DEPTH = 4;
-    double ring[DEPTH];
+    for (int64_t k0 = a; k0 < b; k0 += 32 * D) {
 #pragma unroll
-    for (int u = 0; u < DEPTH; ++u) ring[u] = prod(a + 32 * u + lane);
-    for (int64_t k0 = a; k0 < b; k0 += 32) {
-      const double p = ring[0];
+      for (int u = 0; u < D; ++u) {
+        const int64_t kc = k0 + 32 * u;  // this chunk (warp-uniform)
+        if (kc >= b) break;
+        const double p = __dmul_rn(rv[u], rx[u]);
+        const int64_t kn = kc + 32 * D + lane;  // chunk c+D: its column is in rc[u]
+        rx[u] = kn < b ? x[rc[u]] : 0.0;
+        rv[u] = kn < b ? val[kn] : 0.0;
+        rc[u] = ld_col(kn + 32 * D);
+        const int m = b - kc < 32 ? static_cast<int>(b - kc) : 32;
+        double q[32];  // all 32 broadcasts issued before the dependent adds
 #pragma unroll
-      for (int u = 0; u + 1 < DEPTH; ++u) ring[u] = ring[u + 1];
-      ring[DEPTH - 1] = prod(k0 + 32 * DEPTH + lane);
-      const int m = b - k0 < 32 ? static_cast<int>(b - k0) : 32;
-      double q[32];  // all 32 broadcasts issued before the dependent adds
+        for (int t = 0; t < 32; ++t) q[t] = __shfl_sync(0xffffffffu, p, t);
 #pragma unroll
-      for (int t = 0; t < 32; ++t) q[t] = __shfl_sync(0xffffffffu, p, t);
-#pragma unroll
-      for (int t = 0; t < 32; ++t)
-        if (t < m) acc = __dadd_rn(acc, q[t]);
+        for (int t = 0; t < 32; ++t)
+          if (t < m) acc = __dadd_rn(acc, q[t]);
+      }
     }
     if (lane == 0) y[r] = acc;
   }
