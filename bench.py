@@ -38,9 +38,27 @@ import torch  # noqa: E402
 
 METRIC = "fp64 SpMV GFLOP/s (2*nnz/t), power-iteration step incl. all-gather of x"
 WORKLOADS = {
-    "C5": dict(scale=25, edge_factor=16, seed=105, x_seed=205),
-    "C4": dict(scale=21, edge_factor=10, seed=104, x_seed=204),
+    "C5": dict(scale=25, edge_factor=16, seed=105, x_seed=205, format="csr5"),
+    "C4": dict(scale=21, edge_factor=10, seed=104, x_seed=204, format="csr5"),
+    # BASELINE configs[2]: the 100-iteration power-iteration config (27-point
+    # stencil, 231 MB of ELL > L2); host-generated triplets, ELL by default
+    "C3": dict(host="C3", x_seed=203, format="ell"),
 }
+
+
+def host_csr(name):
+    """Host CSR (ptr, indices, data, n) of a host-generated config through
+    the oracle (the reference's canonicalize / to_csr restated)."""
+    from oracle import port
+
+    from paper_1805_11938_b200 import synth
+
+    cfg = dict(synth.CONFIGS[name])
+    kind = cfg.pop("kind")
+    r, c, v, n = {"laplace2d": synth.laplace2d, "banded": synth.banded, "stencil27": synth.stencil27}[kind](**cfg)
+    row, col, val = port.canonicalize(r, c, v, n, n)
+    ptr, ind, dat = port.to_csr(row, col, val, n)
+    return ptr, ind, dat, n
 # GPU-tuned parameters for the per-format candidates (SURVEY §7.3 item 4);
 # max_cells is raised explicitly above the reference default 2^26 so that
 # SELL can be measured on R-MAT (ELL still cannot: k*n is ~1e13 cells).
@@ -142,8 +160,12 @@ def run_reference(args):
 
     w = WORKLOADS[args.workload]
     cores = port.host_cores()
-    ptr, ind, dat, n_s, n = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"], args.cpu_keep_mod,
-                                                         cores)
+    if "host" in w:  # the whole matrix
+        ptr, ind, dat, n = host_csr(w["host"])
+        n_s = n
+    else:
+        ptr, ind, dat, n_s, n = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
+                                                             args.cpu_keep_mod, cores)
     x = synth_ref.uniform(n, w["x_seed"])
     nnz_s = int(ind.size)
     for _ in range(max(args.warmup, 1)):
@@ -157,7 +179,9 @@ def run_reference(args):
     gflops = 2.0 * nnz_s / t / 1e9
     sample = (f"rows with mix64(r^0xA5A5A5A5) % {args.cpu_keep_mod} == 0 of {args.workload}: {n_s} rows, "
               f"{nnz_s} nnz, full-length x ({n}); spmvkit.kernels.spmv_csr algorithm (oracle/port.py), "
-              f"workers={cores}")
+              f"workers={cores}") if "host" not in w else (
+              f"the whole {args.workload} matrix ({n} rows, {nnz_s} nnz); spmvkit.kernels.spmv_csr algorithm "
+              f"(oracle/port.py), workers={cores}")
     emit({
         "impl": "reference", "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
@@ -173,6 +197,23 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # Our arm
 # --------------------------------------------------------------------------
+def flushed_time(fn, flush, reps: int, warm: int = 3) -> float:
+    """Median seconds of fn() with a 512 MB read (L2 flush) before every
+    rep, each rep bracketed by its own CUDA events."""
+    for _ in range(warm):
+        fn()
+    evs = []
+    for _ in range(reps):
+        flush.sum()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in evs) / 1e3
+
+
 def event_time(fn, reps: int, warm: int = 3) -> float:
     """Average seconds per call of fn() timed with CUDA events on the current stream."""
     for _ in range(warm):
@@ -213,10 +254,20 @@ def run_ours(args):
 
     # ---- build the matrix (untimed setup; conversion times are reported) ----
     t0 = time.perf_counter()
-    r, c, v = synth.rmat_triplets(w["scale"], w["edge_factor"], w["seed"], dev)
+    if "host" in w:
+        cfg = dict(synth.CONFIGS[w["host"]])
+        kind = cfg.pop("kind")
+        hr, hc, hv, n = {"laplace2d": synth.laplace2d, "banded": synth.banded,
+                         "stencil27": synth.stencil27}[kind](**cfg)
+        r = torch.from_numpy(hr).to(dev, torch.int32)
+        c = torch.from_numpy(hc).to(dev, torch.int32)
+        v = torch.from_numpy(hv).to(dev)
+        del hr, hc, hv
+    else:
+        r, c, v = synth.rmat_triplets(w["scale"], w["edge_factor"], w["seed"], dev)
+        n = 1 << w["scale"]
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
-    n = 1 << w["scale"]
     t0 = time.perf_counter()
     a = sp.canonicalize(r, c, v, n, n)
     torch.cuda.synchronize()
@@ -246,7 +297,7 @@ def run_ours(args):
     # ---- per-format candidates on this shard ----
     formats = {}
     best = None
-    wanted = [f.strip() for f in args.formats.split(",") if f.strip()]
+    wanted = [f.strip() for f in (args.formats or w["format"]).split(",") if f.strip()]
     y_tmp = torch.empty(shard.n_rows, dtype=torch.float64, device=dev)
     for tag, kw in CANDIDATES:
         if tag not in wanted:
@@ -288,6 +339,14 @@ def run_ours(args):
             tag = want
             m = sp.convert(tag, shard, **dict(CANDIDATES)[tag])
             t_kernel = event_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), reps=args.kernel_reps)
+
+    # a shard whose format bytes are under 4x L2 would be partly served from
+    # L2 by back-to-back steps: time the kernel and every step after an L2
+    # flush instead
+    flush = None
+    if spmv_bytes(tag, m) < 4 * 126e6:
+        flush = torch.empty(1 << 26, dtype=torch.float64, device=dev)
+        t_kernel = flushed_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), flush, reps=args.kernel_reps)
 
     # ---- roofline of the dominant kernel (this rank's shard) ----
     peak, peak_src = measured_peak()
@@ -372,16 +431,30 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches0 = _lib.load().spmvb_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        pi.step()
-    ev1.record()
-    torch.cuda.synchronize()
+    if flush is None:
+        ev0.record()
+        for _ in range(args.steps):
+            pi.step()
+        ev1.record()
+        torch.cuda.synchronize()
+        t_loop = ev0.elapsed_time(ev1) / 1e3
+    else:  # every step timed on its own after an L2 flush (flush not counted)
+        evs = []
+        for _ in range(args.steps):
+            flush.sum()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            pi.step()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        t_loop = sum(a.elapsed_time(b) for a, b in evs) / 1e3
     if world > 1:
         dist.barrier()
-    launches = _lib.load().spmvb_launch_count() - launches0
+    launches = _lib.load().spmvb_launch_count() - launches0  # the flush is a torch kernel, not counted
     clk = clocks.stop()
-    t_loop = ev0.elapsed_time(ev1) / 1e3
     if world > 1:
         tt = torch.tensor([t_loop], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -458,13 +531,17 @@ def run_ours(args):
         from oracle import cpu_baseline, port, synth_ref
 
         cores = port.host_cores()
-        ptr, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
-                                                             args.cpu_keep_mod, cores)
+        if "host" in w:
+            ptr, ind, dat, n_s = host_csr(w["host"])
+            what = f"the whole matrix ({n_s} rows, {int(ind.size)} nnz)"
+        else:
+            ptr, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
+                                                                 args.cpu_keep_mod, cores)
+            what = f"{n_s} rows (1/{args.cpu_keep_mod} hashed row sample), {int(ind.size)} nnz, full x"
         xs = synth_ref.uniform(n, w["x_seed"])
         tc, reps = cpu_baseline.time_csr(ptr, ind, dat, n_s, xs, cores, min_seconds=args.cpu_seconds)
         cpu = {"value": 2.0 * ind.size / tc / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-               "sample": (f"{n_s} rows (1/{args.cpu_keep_mod} hashed row sample), {int(ind.size)} nnz, full x; "
-                          f"spmvkit spmv_csr algorithm (oracle/port.py), {reps} reps"),
+               "sample": f"{what}; spmvkit spmv_csr algorithm (oracle/port.py), {reps} reps",
                "cpu": cpu_baseline.cpu_model()}
 
     if rank == 0:
@@ -477,7 +554,10 @@ def run_ours(args):
                        "balance": args.balance,
                        "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"
                                 if world > 1 else "y=s*A x; ||y||^2; s=1/||y||"),
-                       "l2": "inputs larger than L2 (matrix >= 6 GB), no flush"},
+                       "l2": (f"inputs larger than L2 ({bytes_model / 1e6:.0f} MB of format bytes per SpMV, "
+                              f"> 4 x 126 MB), no flush" if flush is None else
+                              f"{bytes_model / 1e6:.0f} MB of format bytes per SpMV (< 4 x 126 MB L2): L2 flushed by a "
+                              f"512 MB read before every timed step and kernel rep, each timed on its own")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": f"spmv_{tag} (rank 0 shard)", "bytes_per_launch": bytes_model,
@@ -508,7 +588,7 @@ def main():
     # default is the format that won the full sweep (--formats
     # csr,csr5,hyb,sell,ell; profiles/r01_bench_c5_sweep.json), so the
     # default command is cheap and stable under ncu's serialised replay.
-    ap.add_argument("--formats", default="csr5")
+    ap.add_argument("--formats", default=None)
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--overlap-ranges", type=int, default=4,
