@@ -40,9 +40,12 @@ METRIC = "fp64 SpMV GFLOP/s (2*nnz/t), power-iteration step incl. all-gather of 
 WORKLOADS = {
     "C5": dict(scale=25, edge_factor=16, seed=105, x_seed=205, format="csr5"),
     "C4": dict(scale=21, edge_factor=10, seed=104, x_seed=204, format="csr5"),
-    # BASELINE configs[2]: the 100-iteration power-iteration config (27-point
-    # stencil, 231 MB of ELL > L2); host-generated triplets, ELL by default
+    # BASELINE configs[0..2] (host-generated triplets, ELL by default; under
+    # 4x L2, so timed step by step after an L2 flush): C3 is the
+    # 100-iteration power-iteration config (27-point stencil)
     "C3": dict(host="C3", x_seed=203, format="ell"),
+    "C2": dict(host="C2", x_seed=202, format="ell"),
+    "C1": dict(host="C1", x_seed=201, format="ell"),
 }
 
 
