@@ -331,12 +331,14 @@ def spmv_many(tag: FormatTag, m: FormatMatrix, xs, outs, *, scale=None, ranges: 
     if len(xs) != len(outs):
         raise ValueError(f"{len(xs)} inputs but {len(outs)} outputs")
     for xh in xs:
-        if not (isinstance(xh, torch.Tensor) and not xh.is_cuda and xh.is_pinned() and xh.dtype == torch.float64):
+        if not (isinstance(xh, torch.Tensor) and not xh.is_cuda and xh.dtype == torch.float64
+                and (xh.is_pinned() or xh.numel() == 0)):  # an empty tensor cannot be pinned
             raise ValueError("spmv_many needs pinned float64 CPU tensors (torch.empty(..., pin_memory=True))")
         if xh.numel() != m.n_cols:
             raise ValueError(f"x has length {xh.numel()}, expected {m.n_cols}")
     for yh in outs:
-        if not (isinstance(yh, torch.Tensor) and not yh.is_cuda and yh.is_pinned() and yh.dtype == torch.float64):
+        if not (isinstance(yh, torch.Tensor) and not yh.is_cuda and yh.dtype == torch.float64
+                and (yh.is_pinned() or yh.numel() == 0)):
             raise ValueError("spmv_many needs pinned float64 CPU output tensors")
         if yh.numel() != m.n_rows or not yh.is_contiguous():
             raise ValueError(f"out must be a contiguous tensor of length {m.n_rows}")

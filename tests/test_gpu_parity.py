@@ -406,3 +406,29 @@ def test_spmv_many_pipelined_matches_single_calls(sp, rng, tag, kw):
         assert yh.numpy().tobytes() == want.numpy().tobytes()
     with pytest.raises(ValueError, match="pinned"):
         sp.spmv_many(tag, m, [xs[0].clone()], [ys[0]])
+
+
+def test_new_entry_points_on_degenerate_shapes(sp):
+    """Empty matrices / empty rows through to_coo, spmv_many and the fused
+    push: zeros where the reference gives zeros, no out-of-bounds work."""
+    for nr, nc in [(3, 3), (5, 0), (0, 4), (1, 1)]:
+        rr = np.array([0]) if (nr, nc) == (1, 1) else np.empty(0, dtype=np.int64)
+        a = sp.canonicalize(rr, rr.copy(), np.ones(rr.size), nr, nc)
+        for tag, kw in [("csr", {}), ("csr5", dict(omega=32, sigma=16)), ("ell", {}), ("sell", dict(sell_c=4)),
+                        ("hyb", {})]:
+            m = sp.convert(tag, a, **kw)
+            assert sp.coo_equal(sp.to_coo(m), a), (nr, nc, tag)
+            xs = [torch.ones(nc, dtype=torch.float64).pin_memory() for _ in range(3)]
+            ys = [torch.full((nr,), 7.0, dtype=torch.float64).pin_memory() for _ in range(3)]
+            sp.spmv_many(tag, m, xs, ys)
+            want = sp.spmv(tag, m, torch.ones(nc, dtype=torch.float64, device="cuda")).cpu()
+            for y in ys:
+                assert y.numpy().tobytes() == want.numpy().tobytes(), (nr, nc, tag)
+        if nr > 0 and nc > 0:
+            m5 = sp.to_csr5(a, 32, 16)
+            peer = torch.full((nr + 2,), -1.0, dtype=torch.float64, device="cuda")
+            ptrs = torch.tensor([peer.data_ptr()], dtype=torch.int64, device="cuda")
+            y = sp.spmv_csr5_push(m5, torch.ones(nc, dtype=torch.float64, device="cuda"), None, ptrs, 1)
+            torch.cuda.synchronize()
+            assert peer[1:nr + 1].cpu().numpy().tobytes() == y.cpu().numpy().tobytes()
+            assert float(peer[0]) == -1.0 and float(peer[nr + 1]) == -1.0
