@@ -6,6 +6,7 @@ set -u
 O=gpurun_out
 python -m pytest tests -q -m gpu > $O/final_tests.log 2>&1
 python bench.py > $O/final_bench.json 2> $O/final_bench.err
+for w in C1 C2 C3 C4; do python bench.py --workload $w > $O/final_bench_$w.json 2> $O/final_bench_$w.err; done
 python bench.py --formats csr,csr5,hyb,sell,ell --no-cpu-baseline > $O/final_bench_sweep.json 2> $O/final_sweep.err
 python scripts/bench_formats.py --configs C1,C2,C3,C4 --reps 10 > $O/final_formats.jsonl 2> $O/final_formats.err
 python scripts/bench_convert.py --configs C1,C2,C3,C4,C5 > $O/final_convert.jsonl 2> $O/final_convert.err
