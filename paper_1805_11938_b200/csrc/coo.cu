@@ -25,6 +25,9 @@ struct spmvb_canon {
 
 namespace {
 
+#ifndef SPMVB_PREP_U
+#define SPMVB_PREP_U 4
+#endif
 constexpr int CANON_HIST_COPIES = 4;  // shared-memory digit-count copies per block (warp & 3)
 constexpr int CANON_MAX_PASSES = 8;
 
@@ -44,7 +47,7 @@ __global__ void k_canon_prepare(const I* __restrict__ row, const I* __restrict__
   // input would otherwise put one atomic per entry on a single address.
   // U warp-contiguous groups per thread are loaded before any is used; the
   // previous entry comes from the neighbouring lane (lane 0 loads it).
-  constexpr int U = 4;
+  constexpr int U = SPMVB_PREP_U;
   const int lane = threadIdx.x & 31;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int nc_any = 0;
