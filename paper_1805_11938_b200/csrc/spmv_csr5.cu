@@ -1,6 +1,8 @@
 // CSR5 SpMV (reference kernels.py:139-174 spmv_csr5): per-tile segmented
 // sums over the reference's descriptor layout, warp shuffles across tile
-// columns, and an ordered carry fix-up for rows spanning tiles.
+// columns, and an ordered carry fix-up for rows spanning tiles; plus the
+// row-range and host-buffer entry points and the variant fused with the
+// multi-GPU exchange (rows stored into peer buffers by the same kernel).
 #include <mutex>
 #include <vector>
 
@@ -17,9 +19,9 @@ namespace {
 // =========================================================================
 // CSR5.  Segment ordinal s inside tile t maps to the g-th non-empty row with
 // g = rank(tile_ptr[t]) + s (tile_aux bits 0-30); bit 31 marks a tile whose
-// head continues a row begun earlier: that first segment is a carry.
-// Writing the start segment of non-empty row g also zero-fills the empty
-// rows between non-empty rows g-1 and g (and after the last one).
+// head continues a row begun earlier: that first segment is a carry.  Empty
+// rows receive no segment; the tile kernel's blocks zero them, each a
+// contiguous slice of the row range.
 // =========================================================================
 struct Csr5Ctx {
   int64_t n_rows, nnz, n_nonempty;
