@@ -1,8 +1,11 @@
-// Sparse x exchange for the row-block power iteration:
-// each rank receives only the x entries its shard's columns touch, not the
-// whole all-gathered vector.  Setup finds the shard's column set; every step
-// the owner gathers the requested entries of its y block into one send
-// buffer and the receiver scatters them into its x.
+// Exchange kernels of the row-block power iteration.
+// Sparse x exchange: each rank receives only the x entries its shard's
+// columns touch, not the whole all-gathered vector; setup finds the shard's
+// column set, every step the owner gathers the requested entries of its y
+// block into one send buffer and the receiver scatters them into its x.
+// Peer-memory exchange: rows pushed straight into the peers' buffers
+// (spmvb_push_rows) and the norm slots folded in rank order.  Also the
+// gather-rate probe behind bench.py's roofline.gather_bound.
 #include "spmv_common.cuh"
 
 using namespace spmvb;

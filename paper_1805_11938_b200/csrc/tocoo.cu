@@ -1,8 +1,9 @@
 // Format -> COO triplet extraction on the GPU (reference formats.py:400-453,
 // `to_coo`).  Each function emits triplets that the caller passes through
 // spmvb_canonicalize_*, exactly as the reference routes every format
-// through `canonicalize`; for CSR, CSR5 and ELL the triplets come out in
-// canonical order already, so canonicalize takes its copy-only fast path.
+// through `canonicalize`; every format's triplets come out in canonical
+// order already (SELL through row-order offsets, HYB by merging each row's
+// ELL part and tail), so canonicalize takes its copy-only fast path.
 #include "prims.cuh"
 
 using namespace spmvb;
