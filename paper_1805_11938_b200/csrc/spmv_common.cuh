@@ -122,16 +122,20 @@ __device__ __forceinline__ void fold_chains(int64_t begin, int64_t end, Key key_
 // x gathers are consumed (unpredicated full steps, then a scalar tail).
 // Two alternating buffers: C3 ELL back-to-back 37.5 -> 35.1 us, L2-flushed
 // 43.3 -> 43.1 us, against one buffer copied forward each step.
+template <bool CACHED = false>
 __device__ __forceinline__ double seq_slots(int64_t k, int64_t stride, int64_t base, const int32_t* __restrict__ idx,
                                             const double* __restrict__ val, const double* __restrict__ x) {
+  // CACHED: slot loads through L1 (narrow SELL slices, see seq_slots4)
+  auto li = [](const int32_t* p) { return CACHED ? __ldg(p) : ld_stream(p); };
+  auto lv = [](const double* p) { return CACHED ? __ldg(p) : ld_stream(p); };
   // two 4-slot buffers used alternately (a 2x-unrolled loop) so that no
   // register is copied while its prefetched load is still pending: a
   // copy would wait for the load and end the overlap
   auto load = [&](int64_t j, int32_t (&c)[4], double (&v)[4]) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      c[u] = ld_stream(idx + base + (j + u) * stride);
-      v[u] = ld_stream(val + base + (j + u) * stride);
+      c[u] = li(idx + base + (j + u) * stride);
+      v[u] = lv(val + base + (j + u) * stride);
     }
   };
   double acc = 0.0;
@@ -171,7 +175,7 @@ __device__ __forceinline__ double seq_slots(int64_t k, int64_t stride, int64_t b
   }
   for (; j < k; ++j) {
     const int64_t o = base + j * stride;
-    acc = __dadd_rn(acc, __dmul_rn(ld_stream(val + o), ldx(x, ld_stream(idx + o))));
+    acc = __dadd_rn(acc, __dmul_rn(lv(val + o), ldx(x, li(idx + o))));
   }
   return acc;
 }

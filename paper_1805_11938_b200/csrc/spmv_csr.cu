@@ -261,7 +261,7 @@ void launch_chunk_t(const ChunkArgs& a, cudaStream_t s) {
   }
   if (HAS_ELL) {
     const dim3 g(grid_for(a.n_rows, 256)), b(256);
-    if (a.ell_k > 8)
+    if (a.ell_k >= 8)
       launch_pdl(k_hyb_ell_prepass<true>, g, b, 0, s, a.n_rows, a.ptr, a.ell_k, a.ell_idx, a.ell_val, a.x, a.y,
                  a.scale);
     else

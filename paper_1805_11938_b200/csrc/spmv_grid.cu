@@ -26,9 +26,10 @@ __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict_
 
 // =============================================================== SELL ====
 // MODE 0: four slots per step; 1: the same through L1 (c < 8); 2: with the
-// next four slots prefetched (rows longer than 8 slots).
+// next four slots prefetched (rows of 8 slots or more); 3: prefetched and
+// through L1 (c < 8, rows of 8 slots or more).
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE == 2 ? 5 : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
+__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? 5 : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE == 2 ? 5 : 4)) k_sp
     const int64_t w = widths[sl];
     if (w > SPMVB_SELL_WIDE_COLS && rows_s <= 128) continue;  // k_spmv_sell_wide's slice
     const int64_t base = slice_off[sl] + local;
-    const double acc = MODE == 2 ? seq_slots(w, rows_s, base, idx, val, x)
+    const double acc = MODE >= 2 ? seq_slots<MODE == 3>(w, rows_s, base, idx, val, x)
                                  : seq_slots4<MODE == 1>(w, rows_s, base, idx, val, x);
     const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
     y[r] = scale_p ? s * acc : acc;
@@ -234,8 +235,10 @@ extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths,
     // c < 8: slot loads through L1 (the other half of each index sector is
     // the next slot's); rows of 8 or more slots: next four slots prefetched
     const unsigned g = grid_for(n_rows, 256);
-    auto kern = c < 8 ? k_spmv_sell<1> : (max_narrow_width >= 8 || max_narrow_width < 0) ? k_spmv_sell<2>
-                                                                                        : k_spmv_sell<0>;
+    // (C2 / C3 with the reference default C = 4: mode 3 41.0 / 63.5 ->
+    // 36.9 / 50.2 us L2-flushed against mode 1)
+    const bool wide_rows = max_narrow_width >= 8 || max_narrow_width < 0;
+    auto kern = c < 8 ? (wide_rows ? k_spmv_sell<3> : k_spmv_sell<1>) : (wide_rows ? k_spmv_sell<2> : k_spmv_sell<0>);
     launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
     SPMVB_LAUNCHED("k_spmv_sell");
     if (n_wide > 0) {
