@@ -397,15 +397,26 @@ class PowerIteration:
             self._allgatherv(self.x)
         return self.x
 
-    def run(self, steps: int, graph: bool = False) -> None:
-        """``steps`` power-iteration steps.  ``graph=True`` (single process)
-        captures two steps -- one x/x_next ping-pong -- in a CUDA graph once
-        and replays it, so launch-bound small matrices are not limited by
-        host-side launch cost; an odd remainder step runs eagerly."""
+    def run(self, steps: int, graph: bool | None = None) -> None:
+        """``steps`` power-iteration steps.  Single-process on CUDA (and
+        ``graph`` not False) captures two steps -- one x/x_next ping-pong --
+        in a CUDA graph once and replays it, so launch-bound small matrices
+        are not limited by host-side launch cost; an odd remainder step runs
+        eagerly.  ``graph=None`` (default) picks the graph whenever it
+        applies (not for the p2p exchange, whose symmetric-memory barrier is
+        left eager); iterates are bit-identical to eager steps either way.  If
+        the caller rebinds ``x``/``x_next`` to new tensors the graph is
+        re-captured."""
+        if graph is None:
+            graph = self.exchange != "p2p"
         if not graph or self.world > 1 or self.device.type != "cuda":
             for _ in range(steps):
                 self.step()
             return
+        bufs = (self.x.data_ptr(), self.x_next.data_ptr())
+        g_bufs = getattr(self, "_graph_bufs", None)
+        if getattr(self, "_graph", None) is not None and bufs not in (g_bufs, g_bufs[::-1]):
+            self._graph = None  # buffers were rebound since the capture
         if getattr(self, "_graph", None) is None:
             if steps < 2:
                 for _ in range(steps):
@@ -419,12 +430,12 @@ class PowerIteration:
             torch.cuda.current_stream(self.device).wait_stream(side)
             steps -= 2
             g = torch.cuda.CUDAGraph()
-            self._graph_x = self.x.data_ptr()  # the graph reads this buffer as x
+            self._graph_bufs = (self.x.data_ptr(), self.x_next.data_ptr())  # the graph reads [0] as x
             with torch.cuda.graph(g):
                 self.step()
                 self.step()
             self._graph = g
-        if steps and self.x.data_ptr() != self._graph_x:  # odd step count so far
+        if steps and self.x.data_ptr() != self._graph_bufs[0]:  # odd step count so far
             self.step()
             steps -= 1
         for _ in range(steps // 2):

@@ -114,13 +114,19 @@ def test_power_iteration_graph_replay_identical(sp, rng):
 
         eager = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0)
         graph = spdist.PowerIteration(local, [0, n], 0, 1, torch.device("cuda", 0), x0)
-        eager.run(21)
+        eager.run(21, graph=False)
         graph.run(6, graph=True)
         graph.run(7, graph=True)  # leaves the buffers swapped relative to the capture
-        graph.run(8, graph=True)
+        graph.run(8)  # default: graph replay for a single process
         torch.cuda.synchronize()
         assert torch.equal(eager.x, graph.x), tag
         assert torch.equal(eager.scale, graph.scale), tag
+        # rebinding the iterate to fresh tensors forces a re-capture
+        graph.x, graph.x_next = graph.x.clone(), graph.x_next.clone()
+        eager.run(5, graph=False)
+        graph.run(5)
+        torch.cuda.synchronize()
+        assert torch.equal(eager.x, graph.x), tag
 
 
 @pytest.mark.parametrize("sigma", [16, 8])
