@@ -398,18 +398,29 @@ class PowerIteration:
         return self.x
 
     def run(self, steps: int, graph: bool | None = None) -> None:
-        """``steps`` power-iteration steps.  Single-process on CUDA (and
-        ``graph`` not False) captures two steps -- one x/x_next ping-pong --
-        in a CUDA graph once and replays it, so launch-bound small matrices
-        are not limited by host-side launch cost; an odd remainder step runs
-        eagerly.  ``graph=None`` (default) picks the graph whenever it
-        applies (not for the p2p exchange, whose symmetric-memory barrier is
-        left eager); iterates are bit-identical to eager steps either way.  If
-        the caller rebinds ``x``/``x_next`` to new tensors the graph is
-        re-captured."""
+        """``steps`` power-iteration steps.  ``graph=True`` (single process
+        on CUDA) captures two steps -- one x/x_next ping-pong -- in a CUDA
+        graph once and replays it, so launch-bound small matrices are not
+        limited by host-side launch cost; an odd remainder step runs
+        eagerly.  ``graph=None`` (default) decides by measurement on the
+        first run of at least 14 steps: 4 eager steps and 2 replays (4
+        steps) are timed with CUDA events and the faster mode is kept (the
+        eager chain already overlaps launches with programmatic dependent
+        launch, so GPU-bound matrices gain nothing from the graph).  The
+        p2p exchange, whose symmetric-memory barrier is left eager, and
+        multi-process runs never use the graph.  Iterates are bit-identical
+        either way.  If the caller rebinds ``x``/``x_next`` to new tensors
+        the graph is re-captured."""
+        usable = self.world == 1 and self.device.type == "cuda" and self.exchange != "p2p"
         if graph is None:
-            graph = self.exchange != "p2p"
-        if not graph or self.world > 1 or self.device.type != "cuda":
+            graph = getattr(self, "_graph_auto", None) if usable else False
+            if graph is None:
+                if steps < 14:
+                    graph = False
+                else:
+                    steps = self._calibrate_graph(steps)
+                    graph = self._graph_auto
+        if not graph or not usable:
             for _ in range(steps):
                 self.step()
             return
@@ -442,6 +453,25 @@ class PowerIteration:
             self._graph.replay()
         if steps % 2:
             self.step()
+
+    def _calibrate_graph(self, steps: int) -> int:
+        """Runs 14 of ``steps``: 4 timed eager steps, the graph capture (2
+        warm-up steps, 2 replays) and 2 timed replays; records the faster
+        mode in ``_graph_auto``; returns the steps left."""
+        main = torch.cuda.current_stream(self.device)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(main)
+        for _ in range(4):
+            self.step()
+        e[1].record(main)
+        self._graph = None
+        self.run(6, graph=True)
+        e[2].record(main)
+        self.run(4, graph=True)
+        e[3].record(main)
+        torch.cuda.synchronize(self.device)
+        self._graph_auto = e[2].elapsed_time(e[3]) < e[0].elapsed_time(e[1])
+        return steps - 14
 
     def eigenvalue_estimate(self) -> float:
         """||A x_k|| for the current normalised iterate (1/scale)."""

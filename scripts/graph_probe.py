@@ -32,5 +32,16 @@ for name, tag, kw in [("C1", "ell", {}), ("C2", "ell", {}), ("C3", "ell", {}), (
         torch.cuda.synchronize()
         res[graph] = (e0.elapsed_time(e1) / 100, pi.x.clone())
     same = torch.equal(res[False][1], res[True][1])
+    # the default (graph=None): measured choice on the first long run
+    pi = spdist.PowerIteration(lambda xv, out, s: sp.spmv(tag, m, xv, out=out, scale=s), [0, a.n_rows], 0, 1,
+                               dev, x0)
+    pi.run(20)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pi.run(100)
+    e1.record()
+    torch.cuda.synchronize()
     print(f"{name} {tag}: eager {res[False][0] * 1e3:.1f} us/step, graph {res[True][0] * 1e3:.1f} us/step, "
+          f"default {e0.elapsed_time(e1) * 10:.1f} us/step (graph chosen: {pi._graph_auto}), "
           f"identical iterates {same}", flush=True)

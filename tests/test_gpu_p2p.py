@@ -127,6 +127,13 @@ def test_power_iteration_graph_replay_identical(sp, rng):
         graph.run(5)
         torch.cuda.synchronize()
         assert torch.equal(eager.x, graph.x), tag
+        # the default measures eager vs replay on its first run of >= 14 steps
+        eager.run(23, graph=False)
+        graph.run(23)
+        torch.cuda.synchronize()
+        assert graph._graph_auto in (True, False), tag
+        assert torch.equal(eager.x, graph.x), tag
+        assert torch.equal(eager.scale, graph.scale), tag
 
 
 @pytest.mark.parametrize("sigma", [16, 8])
