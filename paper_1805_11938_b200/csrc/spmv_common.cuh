@@ -5,7 +5,18 @@
 
 namespace spmvb {
 
-__device__ __forceinline__ double ldx(const double* __restrict__ x, int32_t j) { return __ldg(x + j); }
+#ifndef SPMVB_LDX_NOALLOC
+#define SPMVB_LDX_NOALLOC 0  // 1: x gathers bypass L1 allocation (A/B knob)
+#endif
+__device__ __forceinline__ double ldx(const double* __restrict__ x, int32_t j) {
+#if SPMVB_LDX_NOALLOC
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
+  return v;
+#else
+  return __ldg(x + j);
+#endif
+}
 
 __device__ __forceinline__ double load_scale(const double* scale) { return scale ? *scale : 1.0; }
 
