@@ -54,6 +54,12 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     OBJ.mkdir(parents=True, exist_ok=True)
+    # the flags are part of the cache key: objects built with other flags
+    # (an SPMVB_NVCC_EXTRA A/B build) are rebuilt, never silently reused
+    stamp = OBJ / "flags.stamp"
+    flags_key = " ".join(NVCC_FLAGS)
+    if not stamp.exists() or stamp.read_text() != flags_key:
+        force = True
     headers = sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
     sources = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
     jobs = []
@@ -84,6 +90,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
         os.replace(tmp, LIB)
+    stamp.write_text(flags_key)
     return LIB
 
 

@@ -107,6 +107,8 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_column_set": (c_int, [vp, c_i64, c_i64, vp, P_i64, vp]),
     "spmvb_gather_f64": (c_int, [vp, c_i64, vp, c_i64, vp, vp]),
     "spmvb_scatter_f64": (c_int, [vp, vp, c_i64, vp, vp]),
+    "spmvb_degree_order": (c_int, [c_i64, vp, vp, c_i64, vp, vp, P_i64, vp]),
+    "spmvb_relabel_csr": (c_int, [c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp]),
     "spmvb_push_rows": (c_int, [vp, c_i64, vp, c_int, c_i64, vp]),
     "spmvb_sum_inv_sqrt": (c_int, [vp, c_int, vp, vp, vp]),
     "spmvb_gather_probe_threads": (c_i64, []),

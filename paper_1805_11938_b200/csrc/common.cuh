@@ -13,7 +13,6 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <mutex>
-#include <unordered_set>
 #include <string>
 #include <utility>
 
@@ -143,25 +142,9 @@ inline int num_sms() {
 // overlap each launch with the previous kernel's tail.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// SPMVB_CARVEOUT=<0..100> (A/B knob, unset = driver default): the preferred
-// shared-memory carveout applied once to every kernel launched without
-// dynamic shared memory (0 = the largest L1 for the x gathers).
-inline void apply_carveout(const void* fn) {
-  static const int pct = [] {
-    const char* e = std::getenv("SPMVB_CARVEOUT");
-    return e ? std::atoi(e) : -1;
-  }();
-  if (pct < 0) return;
-  static std::mutex mu;
-  static std::unordered_set<const void*> seen;
-  std::lock_guard<std::mutex> g(mu);
-  if (seen.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-}
-
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args... args) {
-  if (smem == 0) apply_carveout(reinterpret_cast<const void*>(kernel));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

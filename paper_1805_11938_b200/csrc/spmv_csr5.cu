@@ -21,7 +21,11 @@ namespace {
 // g = rank(tile_ptr[t]) + s (tile_aux bits 0-30); bit 31 marks a tile whose
 // head continues a row begun earlier: that first segment is a carry.  Empty
 // rows receive no segment; the tile kernel's blocks zero them, each a
-// contiguous slice of the row range.
+// contiguous slice of the row range.  Row lookup: nonempty[g] (the list of
+// non-empty rows), or g itself when nonempty is null -- either no row is
+// empty, or (n_nonempty < n_rows) the non-empty rows are exactly the prefix
+// [0, n_nonempty) and the empty tail is zeroed without any ptr test (the
+// degree-ordered layout of relabel.cu puts every empty row last).
 // =========================================================================
 struct Csr5Ctx {
   int64_t n_rows, nnz, n_nonempty;
@@ -220,9 +224,12 @@ __device__ __forceinline__ void csr5_push_block(const Csr5Ctx& C, const Csr5Push
   const int64_t t1 = t0 + TPB < t_end ? t0 + TPB : t_end;
   const int64_t r0 = t0 <= t_begin ? row_begin : static_cast<int64_t>(C.tile_ptr[t0]);
   const int64_t r1 = t1 >= t_end ? row_end : static_cast<int64_t>(C.tile_ptr[t1]);
-  if (C.nonempty)
+  if (C.nonempty) {
     for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
       if (ld_stream(C.ptr + r) == ld_stream(C.ptr + r + 1)) C.y[r] = 0.0;
+  } else if (C.n_nonempty < C.n_rows) {  // prefix layout: the empty tail
+    for (int64_t r = (r0 > C.n_nonempty ? r0 : C.n_nonempty) + threadIdx.x; r < r1; r += blockDim.x) C.y[r] = 0.0;
+  }
   __syncthreads();
   const int64_t off = P.push_off;
   // pairs (r, r+1) with off + r even: 16-byte aligned in the peer buffers
@@ -250,14 +257,18 @@ __device__ __forceinline__ void csr5_push_block(const Csr5Ctx& C, const Csr5Push
 // of the empty rows of [row_begin, row_end) (a coalesced slice of ptr/y per
 // block), so that streaming pass rides along with the gather-bound tiles
 // instead of costing its own launch.
-template <int W, int S, bool EMPTIES, bool PUSH>
+// MODE: 0 no empty row in the range, 1 empty rows found by ptr tests (the
+// non-empty row list is in use), 2 empty tail [row_begin, row_end) zeroed by
+// plain stores (prefix layout; row_begin is then the first tail row).
+template <int W, int S, int MODE, bool PUSH>
 __device__ __forceinline__ void csr5_tiles(const Csr5Ctx& C, const Csr5Push& P, int64_t t_begin, int64_t t_end,
                                            int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
+  constexpr bool EMPTIES = MODE == 1;
   const int lane = threadIdx.x & 31;
   const int j = lane % W;
   const int64_t group = t_begin + (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / W;
-  const int64_t zr0 = EMPTIES ? row_begin + blockIdx.x * rows_per_block : 0;
-  const int64_t zr1 = EMPTIES ? (zr0 + rows_per_block < row_end ? zr0 + rows_per_block : row_end) : 0;
+  const int64_t zr0 = MODE != 0 ? row_begin + blockIdx.x * rows_per_block : 0;
+  const int64_t zr1 = MODE != 0 ? (zr0 + rows_per_block < row_end ? zr0 + rows_per_block : row_end) : 0;
   // This block's slice of the empty rows: the ptr pairs of its first ZP
   // rows per thread are loaded up front with the tile's streams (ptr is not
   // written by the predecessor kernel) and tested/zeroed after the tile's
@@ -276,8 +287,8 @@ __device__ __forceinline__ void csr5_tiles(const Csr5Ctx& C, const Csr5Push& P, 
     zp0[k] = r < zr1 ? ld_stream(C.ptr + r) : 0;
     zp1[k] = r < zr1 ? ld_stream(C.ptr + r + 1) : 0;
   }
-  auto zero_empty_rows_first = [&] {  // !EMPTIES only (see above)
-    if (rows_per_block > 0) {
+  auto zero_empty_rows_first = [&] {  // MODE 0 only (see above)
+    if (MODE == 0 && rows_per_block > 0) {
       const int64_t r0 = row_begin + blockIdx.x * rows_per_block;
       const int64_t r1 = r0 + rows_per_block < row_end ? r0 + rows_per_block : row_end;
       for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x)
@@ -286,6 +297,9 @@ __device__ __forceinline__ void csr5_tiles(const Csr5Ctx& C, const Csr5Push& P, 
   };
   auto zero_row = [&](int64_t r) { C.y[r] = 0.0; };
   auto zero_empty_rows = [&] {
+    if (MODE == 2) {  // the block's slice of the empty tail
+      for (int64_t r = zr0 + threadIdx.x; r < zr1; r += blockDim.x) zero_row(r);
+    }
     if (EMPTIES && rows_per_block > 0) {
       int64_t r = zr0 + threadIdx.x;
 #pragma unroll
@@ -373,10 +387,10 @@ __device__ __forceinline__ void csr5_tiles(const Csr5Ctx& C, const Csr5Push& P, 
   if constexpr (PUSH) csr5_push_block<W>(C, P, t_begin, t_end, row_begin, row_end);
 }
 
-template <int W, int S, bool EMPTIES>
+template <int W, int S, int MODE>
 __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s(Csr5Ctx C, int64_t t_begin, int64_t t_end,
                                                      int64_t rows_per_block, int64_t row_begin, int64_t row_end) {
-  csr5_tiles<W, S, EMPTIES, false>(C, Csr5Push{}, t_begin, t_end, rows_per_block, row_begin, row_end);
+  csr5_tiles<W, S, MODE, false>(C, Csr5Push{}, t_begin, t_end, rows_per_block, row_begin, row_end);
 }
 
 // The same tiles fused with the exchange (csr5_push_block epilogue).
@@ -384,7 +398,7 @@ template <int W, int S>
 __global__ void __launch_bounds__(256, SPMVB_CSR5_MINB) k_csr5_warp_s_push(Csr5Ctx C, Csr5Push P, int64_t t_begin,
                                                                           int64_t t_end, int64_t row_begin,
                                                                           int64_t row_end) {
-  csr5_tiles<W, S, false, true>(C, P, t_begin, t_end, 0, row_begin, row_end);
+  csr5_tiles<W, S, 0, true>(C, P, t_begin, t_end, 0, row_begin, row_end);
 }
 
 // Carry fix-up of the continuation chains (consecutive tiles whose head
@@ -421,10 +435,13 @@ __global__ void k_csr5_fixup(int64_t t_begin, int64_t t_end, const int32_t* __re
 void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_begin, int64_t row_end,
                   cudaStream_t s, const Csr5Push& P = Csr5Push{}) {
   const bool empties = C.nonempty && row_end > row_begin;
+  // prefix layout: rows [tail0, row_end) of the range are empty
+  const int64_t tail0 = C.n_nonempty > row_begin ? C.n_nonempty : row_begin;
+  const bool tail = !C.nonempty && C.n_nonempty < C.n_rows && row_end > tail0;
   auto empty_pass = [&] {
-    if (empties) {
-      k_csr5_empty_rows<<<grid_for(row_end - row_begin, 256, 148 * 32), 256, 0, s>>>(
-          row_end - row_begin, C.ptr + row_begin, C.y + row_begin);
+    if (empties || tail) {
+      const int64_t z0 = empties ? row_begin : tail0;
+      k_csr5_empty_rows<<<grid_for(row_end - z0, 256, 148 * 32), 256, 0, s>>>(row_end - z0, C.ptr + z0, C.y + z0);
       SPMVB_LAUNCHED("k_csr5_empty_rows");
     }
   };
@@ -444,12 +461,18 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
       generic_begin = fe;
     }
   };
-  auto warp_s_launch = [&](auto kern_e, auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
+  auto warp_s_launch = [&](auto kern_e, auto kern_t, auto kern, int W) {  // every tile incl. the partial one, plus the empty rows
     const int64_t blocks = ((t_end - t_begin) * W + 255) / 256;
-    const int64_t rpb = empties ? (row_end - row_begin + blocks - 1) / blocks : 0;
-    if (rpb > 0) kern = kern_e;
-    launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, C, t_begin, t_end, rpb, row_begin,
-               row_end);
+    int64_t rpb = 0, z0 = row_begin;
+    if (empties) {
+      rpb = (row_end - row_begin + blocks - 1) / blocks;
+      kern = kern_e;
+    } else if (tail) {
+      z0 = tail0;
+      rpb = (row_end - tail0 + blocks - 1) / blocks;
+      kern = kern_t;
+    }
+    launch_pdl(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, C, t_begin, t_end, rpb, z0, row_end);
     SPMVB_LAUNCHED("k_csr5_warp_s");
     generic_begin = t_end;
   };
@@ -465,17 +488,17 @@ void launch_range(const Csr5Ctx& C, int64_t t_begin, int64_t t_end, int64_t row_
   } else if ((sigma == 16 || sigma == 8) && (omega == 32 || omega == 16 || omega == 8 || omega == 4)) {
     if (sigma == 16) {
       switch (omega) {
-        case 32: warp_s_launch(k_csr5_warp_s<32, 16, true>, k_csr5_warp_s<32, 16, false>, 32); break;
-        case 16: warp_s_launch(k_csr5_warp_s<16, 16, true>, k_csr5_warp_s<16, 16, false>, 16); break;
-        case 8: warp_s_launch(k_csr5_warp_s<8, 16, true>, k_csr5_warp_s<8, 16, false>, 8); break;
-        default: warp_s_launch(k_csr5_warp_s<4, 16, true>, k_csr5_warp_s<4, 16, false>, 4); break;
+        case 32: warp_s_launch(k_csr5_warp_s<32, 16, 1>, k_csr5_warp_s<32, 16, 2>, k_csr5_warp_s<32, 16, 0>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 16, 1>, k_csr5_warp_s<16, 16, 2>, k_csr5_warp_s<16, 16, 0>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 16, 1>, k_csr5_warp_s<8, 16, 2>, k_csr5_warp_s<8, 16, 0>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 16, 1>, k_csr5_warp_s<4, 16, 2>, k_csr5_warp_s<4, 16, 0>, 4); break;
       }
     } else {
       switch (omega) {
-        case 32: warp_s_launch(k_csr5_warp_s<32, 8, true>, k_csr5_warp_s<32, 8, false>, 32); break;
-        case 16: warp_s_launch(k_csr5_warp_s<16, 8, true>, k_csr5_warp_s<16, 8, false>, 16); break;
-        case 8: warp_s_launch(k_csr5_warp_s<8, 8, true>, k_csr5_warp_s<8, 8, false>, 8); break;
-        default: warp_s_launch(k_csr5_warp_s<4, 8, true>, k_csr5_warp_s<4, 8, false>, 4); break;
+        case 32: warp_s_launch(k_csr5_warp_s<32, 8, 1>, k_csr5_warp_s<32, 8, 2>, k_csr5_warp_s<32, 8, 0>, 32); break;
+        case 16: warp_s_launch(k_csr5_warp_s<16, 8, 1>, k_csr5_warp_s<16, 8, 2>, k_csr5_warp_s<16, 8, 0>, 16); break;
+        case 8: warp_s_launch(k_csr5_warp_s<8, 8, 1>, k_csr5_warp_s<8, 8, 2>, k_csr5_warp_s<8, 8, 0>, 8); break;
+        default: warp_s_launch(k_csr5_warp_s<4, 8, 1>, k_csr5_warp_s<4, 8, 2>, k_csr5_warp_s<4, 8, 0>, 4); break;
       }
     }
   } else if (sigma <= 1024 && (omega == 32 || omega == 16 || omega == 8 || omega == 4 || omega == 2)) {

@@ -397,25 +397,28 @@ class PowerIteration:
             self._allgatherv(self.x)
         return self.x
 
-    def run(self, steps: int, graph: bool | None = None) -> None:
-        """``steps`` power-iteration steps.  ``graph=True`` (single process
-        on CUDA) captures two steps -- one x/x_next ping-pong -- in a CUDA
-        graph once and replays it, so launch-bound small matrices are not
-        limited by host-side launch cost; an odd remainder step runs
-        eagerly.  ``graph=None`` (default) decides by measurement on the
-        first run of at least 14 steps: 4 eager steps and 2 replays (4
-        steps) are timed with CUDA events and the faster mode is kept (the
-        eager chain already overlaps launches with programmatic dependent
-        launch, so GPU-bound matrices gain nothing from the graph).  The
-        p2p exchange, whose symmetric-memory barrier is left eager, and
-        multi-process runs never use the graph.  Iterates are bit-identical
-        either way.  If the caller rebinds ``x``/``x_next`` to new tensors
-        the graph is re-captured."""
+    def run(self, steps: int, graph: bool | str = False) -> None:
+        """``steps`` power-iteration steps, eagerly by default.
+
+        ``graph=True`` (single process on CUDA, opt-in) captures two steps --
+        one x/x_next ping-pong -- in a CUDA graph once and replays it, so
+        launch-bound small matrices are not limited by host-side launch cost;
+        an odd remainder step runs eagerly.  Capture contract: ``local_spmv``
+        must not synchronise with the host (no host x/out, no ``.item()``)
+        and must keep reading and writing the same buffers on every call
+        (its matrix, scale and output pointers are frozen into the graph).
+        Rebinding ``x``/``x_next`` is detected and re-captures; if capture
+        fails the steps run eagerly (with a warning) and the iterate is left
+        as eager steps would leave it.  ``graph="auto"`` times alternating
+        rounds of eager steps and replays once (median of 3 each) and keeps
+        the faster mode.  The p2p exchange (its symmetric-memory barrier is
+        left eager) and multi-process runs never use the graph.  Iterates are
+        bit-identical either way."""
         usable = self.world == 1 and self.device.type == "cuda" and self.exchange != "p2p"
-        if graph is None:
+        if graph == "auto":
             graph = getattr(self, "_graph_auto", None) if usable else False
             if graph is None:
-                if steps < 14:
+                if steps < 16:
                     graph = False
                 else:
                     steps = self._calibrate_graph(steps)
@@ -441,10 +444,22 @@ class PowerIteration:
             torch.cuda.current_stream(self.device).wait_stream(side)
             steps -= 2
             g = torch.cuda.CUDAGraph()
-            self._graph_bufs = (self.x.data_ptr(), self.x_next.data_ptr())  # the graph reads [0] as x
-            with torch.cuda.graph(g):
-                self.step()
-                self.step()
+            state = (self.x, self.x_next, self.sumsq.clone(), self.scale.clone())
+            captured = (self.x.data_ptr(), self.x_next.data_ptr())
+            err = self._capture(g)
+            if err is not None:  # not capturable: restore the pre-capture state, run eagerly
+                import warnings
+
+                self.x, self.x_next = state[0], state[1]
+                self.sumsq.copy_(state[2])
+                self.scale.copy_(state[3])
+                warnings.warn(f"PowerIteration: CUDA graph capture failed ({type(err).__name__}: {err}); "
+                              "running eager steps", RuntimeWarning, stacklevel=2)
+                self._graph = None
+                for _ in range(steps):
+                    self.step()
+                return
+            self._graph_bufs = captured  # the graph reads [0] as x
             self._graph = g
         if steps and self.x.data_ptr() != self._graph_bufs[0]:  # odd step count so far
             self.step()
@@ -454,24 +469,72 @@ class PowerIteration:
         if steps % 2:
             self.step()
 
+    def _capture(self, g) -> Exception | None:
+        """Captures two steps into ``g`` on a side stream; returns the error
+        if the steps could not be captured.  (Done by hand rather than with
+        ``torch.cuda.graph``: when a capture is invalidated its exit raises
+        before it restores the current stream and before the caching
+        allocator stops routing allocations to the graph's pool.)"""
+        dev = self.device
+        pool = torch.cuda.graph_pool_handle()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        err = None
+        with torch.cuda.stream(side):
+            g.capture_begin(pool=pool)
+            try:
+                self.step()
+                self.step()
+            except Exception as exc:
+                err = exc
+            try:
+                g.capture_end()
+            except Exception as exc:
+                err = err or exc
+                torch._C._cuda_endAllocateToPool(dev.index if dev.index is not None else torch.cuda.current_device(),
+                                                 pool)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        if err is not None:
+            torch.cuda.synchronize(dev)
+        return err
+
     def _calibrate_graph(self, steps: int) -> int:
-        """Runs 14 of ``steps``: 4 timed eager steps, the graph capture (2
-        warm-up steps, 2 replays) and 2 timed replays; records the faster
-        mode in ``_graph_auto``; returns the steps left."""
+        """Runs 16 of ``steps``: the capture (2 warm-up steps, 2 replays),
+        then three alternating rounds of 2 timed eager steps and 1 timed
+        replay (2 steps); keeps the mode with the smaller median in
+        ``_graph_auto`` and drops the graph when eager wins.  Returns the
+        steps left."""
         main = torch.cuda.current_stream(self.device)
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e[0].record(main)
-        for _ in range(4):
-            self.step()
-        e[1].record(main)
         self._graph = None
-        self.run(6, graph=True)
-        e[2].record(main)
         self.run(4, graph=True)
-        e[3].record(main)
+        if getattr(self, "_graph", None) is None:  # capture failed: eager
+            self._graph_auto = False
+            return steps - 4
+        if self.x.data_ptr() != self._graph_bufs[0]:
+            self.step()
+            steps -= 1
+        ev = []
+        for _ in range(3):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record(main)
+            self.step()
+            self.step()
+            e[1].record(main)
+            self._graph.replay()
+            e[2].record(main)
+            ev.append(e)
         torch.cuda.synchronize(self.device)
-        self._graph_auto = e[2].elapsed_time(e[3]) < e[0].elapsed_time(e[1])
-        return steps - 14
+        eager = sorted(e[0].elapsed_time(e[1]) for e in ev)[1]
+        replay = sorted(e[1].elapsed_time(e[2]) for e in ev)[1]
+        self._graph_auto = replay < eager
+        if not self._graph_auto:
+            self._graph = None  # release the graph and its private pool
+        return steps - 16
+
+    def normalized(self) -> torch.Tensor:
+        """The unit-norm iterate ``scale * x`` (``x`` holds the last SpMV
+        output; its normalisation is deferred into the next SpMV)."""
+        return self.x * self.scale
 
     def eigenvalue_estimate(self) -> float:
         """||A x_k|| for the current normalised iterate (1/scale)."""

@@ -412,6 +412,11 @@ def to_csr5(a, omega: int, sigma: int) -> Csr5Matrix:
         if nnz and nonempty < csr.n_rows:
             rows = _i32(nonempty, dev)
             check(LIB.spmvb_csr_nonempty_rows(ptr(csr.ptr), csr.n_rows, ptr(rows), s))
+            if int(rows[-1].item()) == nonempty - 1:
+                # the non-empty rows are the prefix [0, nonempty) (e.g. the
+                # degree-ordered layout of relabel.py): no row lookup, the
+                # empty tail is zeroed without ptr tests (spmvb.h)
+                rows = None
         # kernel-side: the flags packed one bit per entry (64 B per 512-entry tile)
         bits = _i32((nnz + 31) // 32, dev)
         check(LIB.spmvb_csr5_pack_flags(nnz, ptr(bit_flag), ptr(bits), s))

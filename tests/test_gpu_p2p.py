@@ -117,23 +117,52 @@ def test_power_iteration_graph_replay_identical(sp, rng):
         eager.run(21, graph=False)
         graph.run(6, graph=True)
         graph.run(7, graph=True)  # leaves the buffers swapped relative to the capture
-        graph.run(8)  # default: graph replay for a single process
+        graph.run(8, graph=True)
         torch.cuda.synchronize()
         assert torch.equal(eager.x, graph.x), tag
         assert torch.equal(eager.scale, graph.scale), tag
         # rebinding the iterate to fresh tensors forces a re-capture
         graph.x, graph.x_next = graph.x.clone(), graph.x_next.clone()
         eager.run(5, graph=False)
-        graph.run(5)
+        graph.run(5, graph=True)
         torch.cuda.synchronize()
         assert torch.equal(eager.x, graph.x), tag
-        # the default measures eager vs replay on its first run of >= 14 steps
+        # "auto" measures eager vs replay on its first run of >= 16 steps
         eager.run(23, graph=False)
-        graph.run(23)
+        graph.run(23, graph="auto")
         torch.cuda.synchronize()
         assert graph._graph_auto in (True, False), tag
         assert torch.equal(eager.x, graph.x), tag
         assert torch.equal(eager.scale, graph.scale), tag
+        # the default is eager
+        eager.run(3)
+        graph.run(3)
+        torch.cuda.synchronize()
+        assert torch.equal(eager.x, graph.x), tag
+
+
+def test_power_iteration_graph_capture_failure_falls_back(sp, rng):
+    """A local_spmv that syncs with the host cannot be captured: run(graph=True)
+    warns and finishes eagerly with the same iterate as eager steps."""
+    from paper_1805_11938_b200 import dist as spdist
+
+    r, c, v = sp.synth.rmat_triplets(scale=10, edge_factor=8, seed=7)
+    n = 1 << 10
+    m = sp.to_csr5(sp.canonicalize(r, c, v, n, n), 32, 16)
+    x0 = torch.from_numpy(rng.uniform(0.5, 1.0, size=n)).cuda()
+
+    def syncing(xv, out, scale):
+        sp.spmv("csr5", m, xv, out=out, scale=scale)
+        float(out[0].item())  # host sync: illegal inside a capture
+
+    eager = spdist.PowerIteration(syncing, [0, n], 0, 1, torch.device("cuda", 0), x0)
+    graph = spdist.PowerIteration(syncing, [0, n], 0, 1, torch.device("cuda", 0), x0)
+    eager.run(9)
+    with pytest.warns(RuntimeWarning, match="capture failed"):
+        graph.run(9, graph=True)
+    torch.cuda.synchronize()
+    assert torch.equal(eager.x, graph.x)
+    assert torch.equal(eager.scale, graph.scale)
 
 
 @pytest.mark.parametrize("sigma", [16, 8])
