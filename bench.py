@@ -580,6 +580,35 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def launch_ranks(args):
+    """--gpus N: one rank per GPU.  Under torchrun (WORLD_SIZE set) the world
+    must be N; without it, N > 1 re-executes this command under
+    torch.distributed.run with N local ranks on 127.0.0.1 (NCCL's init
+    messages stay on stderr), after checking that N GPUs are visible."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU\n")
+            sys.exit(2)
+        return
+    if args.gpus == 1:
+        return
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}\n")
+        sys.exit(2)
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.stderr.write("bench.py: launching " + " ".join(cmd) + "\n")
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -610,6 +639,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.impl == "ours":
+        launch_ranks(args)
     _isolate_stdout()
     if args.impl == "reference":
         run_reference(args)

@@ -33,10 +33,11 @@ def _lib():
     if not SO.exists():
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     lib = ctypes.CDLL(str(SO))
-    lib.rmat_sample.restype = ctypes.c_int64
-    lib.rmat_sample.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
-                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    lib.rmat_sample_ranges.restype = ctypes.c_int64
+    lib.rmat_sample_ranges.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p,
+                                       ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     return lib
 
 
@@ -46,19 +47,28 @@ def kept_rows(n: int, keep_mod: int) -> np.ndarray:
     return np.nonzero(h % np.uint64(keep_mod) == 0)[0].astype(np.int64)
 
 
-def rmat_row_sample(scale: int, edge_factor: int, seed: int, keep_mod: int, threads: int | None = None):
-    """CSR (ptr, indices, data) of the sampled rows (compressed), n_cols = 2^scale."""
+def rmat_row_subset(scale: int, edge_factor: int, seed: int, keep_mod: int = 0, ranges=(),
+                    threads: int | None = None):
+    """Canonical rows of the R-MAT matrix (first-draw dedup, as the GPU
+    generator) for the hashed 1/keep_mod row sample (keep_mod 0: none) plus
+    every row in the half-open ``ranges``: returns (rows, ptr, ind, dat),
+    ``rows`` the ascending global row ids, CSR over them (compressed), all
+    columns global."""
     threads = threads or port.host_cores()
     lib = _lib()
+    n = 1 << scale
     draws = edge_factor << scale
-    cap = int(draws / keep_mod * 1.3) + (1 << 20)
+    rng = np.ascontiguousarray(np.asarray(ranges, dtype=np.int32).reshape(-1, 2))
+    span = int((rng[:, 1] - rng[:, 0]).clip(0).sum()) if rng.size else 0
+    cap = (int(draws / keep_mod * 1.3) if keep_mod else 0) + (1 << 20)
     while True:
         e = np.empty(cap, np.int64)
         r = np.empty(cap, np.int32)
         c = np.empty(cap, np.int32)
         v = np.empty(cap, np.float64)
-        total = lib.rmat_sample(scale, draws, 0.57, 0.19, 0.19, seed, keep_mod, cap, e.ctypes.data, r.ctypes.data,
-                                c.ctypes.data, v.ctypes.data, threads)
+        total = lib.rmat_sample_ranges(scale, draws, 0.57, 0.19, 0.19, seed, keep_mod,
+                                       rng.ctypes.data if rng.size else None, int(rng.shape[0]), cap,
+                                       e.ctypes.data, r.ctypes.data, c.ctypes.data, v.ctypes.data, threads)
         if total <= cap:
             break
         cap = int(total) + 1
@@ -66,12 +76,19 @@ def rmat_row_sample(scale: int, edge_factor: int, seed: int, keep_mod: int, thre
     key = (r << scale) | c
     _, first = np.unique(key, return_index=True)  # draws ascend: index = first draw
     r, c, v = r[first], c[first], v[first]
-    rows = kept_rows(1 << scale, keep_mod)
+    parts = [kept_rows(n, keep_mod)] if keep_mod else []
+    parts += [np.arange(lo, hi, dtype=np.int64) for lo, hi in rng]
+    rows = np.unique(np.concatenate(parts)) if parts else np.empty(0, np.int64)
     local = np.searchsorted(rows, r)
-    n_s = rows.size
-    lr, lc, lv = port.canonicalize(local, c, v, n_s, 1 << scale)
-    ptr, ind, dat = port.to_csr(lr, lc, lv, n_s)
-    return ptr, ind, dat, n_s, 1 << scale
+    lr, lc, lv = port.canonicalize(local, c, v, rows.size, n)
+    ptr, ind, dat = port.to_csr(lr, lc, lv, rows.size)
+    return rows, ptr, ind, dat
+
+
+def rmat_row_sample(scale: int, edge_factor: int, seed: int, keep_mod: int, threads: int | None = None):
+    """CSR (ptr, indices, data) of the sampled rows (compressed), n_cols = 2^scale."""
+    rows, ptr, ind, dat = rmat_row_subset(scale, edge_factor, seed, keep_mod, (), threads)
+    return ptr, ind, dat, rows.size, 1 << scale
 
 
 def time_csr(ptr, ind, dat, n_rows, x, workers: int, min_seconds: float = 8.0, min_reps: int = 3,

@@ -4,6 +4,9 @@
  * (paper_1805_11938_b200/csrc/gen.cu) with the same counter hash and keeps
  * only draws whose row r satisfies mix64(r ^ 0xA5A5A5A5) % keep_mod == 0,
  * i.e. an unbiased 1/keep_mod sample of the rows of the full R-MAT matrix.
+ * rmat_sample_ranges() additionally keeps every row inside any of a list of
+ * half-open row ranges (the contiguous row windows behind a CSR5 tile
+ * window, tests/test_gpu_c5_oracle.py).
  * Output: draws in ascending draw order (deduplication is done by the
  * caller, keeping the first draw as the GPU generator does).
  *
@@ -33,6 +36,8 @@ typedef struct {
   uint64_t sm;
   double a, ab, abc;
   uint32_t keep_mod;
+  const int32_t* ranges; /* n_ranges pairs [lo, hi) */
+  int n_ranges;
   int64_t* buf;
   int64_t* e_out;
   int32_t *row_out, *col_out;
@@ -47,7 +52,10 @@ static void* scan_rows(void* p) {
   for (int64_t e = j->lo; e < j->hi; ++e) {
     uint32_t row = 0;
     for (int l = 0; l < j->scale; ++l) row = (row << 1) | (u01(j->sm, (uint64_t)e, l) >= j->ab ? 1u : 0u);
-    if (!rmat_row_keep((int32_t)row, j->keep_mod)) continue;
+    int keep = j->keep_mod > 0 && rmat_row_keep((int32_t)row, j->keep_mod);
+    for (int q = 0; q < j->n_ranges && !keep; ++q)
+      keep = (int32_t)row >= j->ranges[2 * q] && (int32_t)row < j->ranges[2 * q + 1];
+    if (!keep) continue;
     if (j->n == j->cap) {
       j->cap *= 2;
       j->buf = (int64_t*)realloc(j->buf, (size_t)j->cap * sizeof(int64_t));
@@ -78,10 +86,11 @@ static void* emit(void* p) {
   return NULL;
 }
 
-/* Returns the number of sampled draws; writes at most max_out of them. */
-int64_t rmat_sample(int scale, int64_t draws, double a, double b, double c, uint64_t seed, uint32_t keep_mod,
-                    int64_t max_out, int64_t* e_out, int32_t* row_out, int32_t* col_out, double* val_out,
-                    int nthreads) {
+/* Returns the number of sampled draws; writes at most max_out of them.
+ * keep_mod == 0 keeps no hashed rows (ranges only). */
+int64_t rmat_sample_ranges(int scale, int64_t draws, double a, double b, double c, uint64_t seed,
+                           uint32_t keep_mod, const int32_t* ranges, int n_ranges, int64_t max_out,
+                           int64_t* e_out, int32_t* row_out, int32_t* col_out, double* val_out, int nthreads) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   Job jobs[256];
@@ -97,6 +106,8 @@ int64_t rmat_sample(int scale, int64_t draws, double a, double b, double c, uint
     j->ab = a + b;
     j->abc = a + b + c;
     j->keep_mod = keep_mod;
+    j->ranges = ranges;
+    j->n_ranges = n_ranges;
     j->max_out = max_out;
     j->e_out = e_out;
     j->row_out = row_out;
@@ -116,4 +127,11 @@ int64_t rmat_sample(int scale, int64_t draws, double a, double b, double c, uint
   }
   for (int t = 0; t < nthreads; ++t) free(jobs[t].buf);
   return total;
+}
+
+int64_t rmat_sample(int scale, int64_t draws, double a, double b, double c, uint64_t seed, uint32_t keep_mod,
+                    int64_t max_out, int64_t* e_out, int32_t* row_out, int32_t* col_out, double* val_out,
+                    int nthreads) {
+  return rmat_sample_ranges(scale, draws, a, b, c, seed, keep_mod, NULL, 0, max_out, e_out, row_out, col_out,
+                            val_out, nthreads);
 }

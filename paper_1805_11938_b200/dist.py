@@ -150,6 +150,8 @@ class PowerIteration:
                  local_spmv_push: Callable | None = None):
         if exchange not in ("allgatherv", "sparse", "p2p"):
             raise ValueError(f"unknown exchange {exchange!r}")
+        if exchange == "p2p" and world > 1 and dist.get_backend(group) == dist.Backend.GLOO:
+            raise ValueError("exchange='p2p' needs NCCL and peer-mapped GPUs, not gloo")
         self.local_spmv = local_spmv
         self.bounds = [int(b) for b in bounds]
         self.rank, self.world = rank, world
@@ -162,6 +164,11 @@ class PowerIteration:
         self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
         self.scale = torch.ones(1, dtype=torch.float64, device=device)
         self.lo, self.hi = self.bounds[rank], self.bounds[rank + 1]
+        # device tensors over a backend without a device transport (gloo):
+        # every exchange is staged through a host copy of the iterate
+        self._staged = (device.type == "cuda" and world > 1 and
+                        dist.get_backend(self.group) == dist.Backend.GLOO)
+        self._host = torch.empty(n if self._staged else 0, dtype=torch.float64, pin_memory=self._staged)
         # p2p also runs at world 1 (no peers: it exercises the buffers,
         # barrier and norm slots on one GPU)
         self.exchange = exchange if (world > 1 or exchange == "p2p") else "allgatherv"
@@ -191,7 +198,26 @@ class PowerIteration:
             self._spans = allspans
 
     # ---- full exchange ---------------------------------------------------
+    def _all_reduce_sumsq(self) -> None:
+        if self._staged:
+            s = self.sumsq.cpu()
+            dist.all_reduce(s, group=self.group)
+            self.sumsq.copy_(s)
+        else:
+            dist.all_reduce(self.sumsq, group=self.group)
+
     def _allgatherv(self, y_full: torch.Tensor) -> None:
+        if self._staged:  # exchange host copies, then upload the peers' rows
+            self._host[self.lo:self.hi].copy_(y_full[self.lo:self.hi])
+            self._allgatherv_tensor(self._host)
+            for p in range(self.world):
+                lo, hi = self.bounds[p], self.bounds[p + 1]
+                if p != self.rank and hi > lo:
+                    y_full[lo:hi].copy_(self._host[lo:hi])
+            return
+        self._allgatherv_tensor(y_full)
+
+    def _allgatherv_tensor(self, y_full: torch.Tensor) -> None:
         mine = y_full[self.lo : self.hi]
         ops = []
         for p in range(self.world):
@@ -213,12 +239,14 @@ class PowerIteration:
         cuts = np.searchsorted(need.cpu().numpy(), self.bounds, side="left")
         recv_counts = [int(cuts[q + 1] - cuts[q]) if q != me else 0 for q in range(P)]
         # counts matrix: row p = what rank p receives from each owner
-        mine = torch.tensor(recv_counts, dtype=torch.int64, device=self.device)
+        xdev = torch.device("cpu") if self._staged else self.device  # where the collectives run
+        mine = torch.tensor(recv_counts, dtype=torch.int64, device=xdev)
         allc = [torch.empty_like(mine) for _ in range(P)]
         dist.all_gather(allc, mine, group=self.group)
         send_counts = [int(allc[p][me].item()) if p != me else 0 for p in range(P)]
         # request lists: rank p tells owner q which of q's rows it reads
-        send_idx = torch.empty(sum(send_counts), dtype=torch.int32, device=self.device)
+        send_idx = torch.empty(sum(send_counts), dtype=torch.int32, device=xdev)
+        need_x = need.to(xdev)
         ops, s_off, r_off = [], [0], [0]
         for p in range(P):
             s_off.append(s_off[-1] + send_counts[p])
@@ -227,7 +255,7 @@ class PowerIteration:
             if p == me:
                 continue
             if recv_counts[p]:
-                ops.append(dist.P2POp(dist.isend, need[int(cuts[p]):int(cuts[p + 1])].contiguous(), p,
+                ops.append(dist.P2POp(dist.isend, need_x[int(cuts[p]):int(cuts[p + 1])].contiguous(), p,
                                       group=self.group))
             if send_counts[p]:
                 ops.append(dist.P2POp(dist.irecv, send_idx[s_off[p]:s_off[p + 1]], p, group=self.group))
@@ -236,11 +264,14 @@ class PowerIteration:
                 req.wait()
         self._recv_idx = torch.cat([need[int(cuts[q]):int(cuts[q + 1])] for q in range(P) if q != me]) \
             if P > 1 else need[:0]
-        self._send_idx = send_idx
+        self._send_idx = send_idx.to(self.device)
         self._send_counts, self._recv_counts = send_counts, recv_counts
         self._s_off, self._r_off = s_off, r_off
         self._send_buf = torch.empty(max(s_off[-1], 1), dtype=torch.float64, device=self.device)
         self._recv_buf = torch.empty(max(r_off[-1], 1), dtype=torch.float64, device=self.device)
+        if self._staged:
+            self._send_host = torch.empty(self._send_buf.numel(), dtype=torch.float64, pin_memory=True)
+            self._recv_host = torch.empty(self._recv_buf.numel(), dtype=torch.float64, pin_memory=True)
         self.exchange_volume = {"send_entries": s_off[-1], "recv_entries": r_off[-1],
                                 "allgatherv_recv_entries": n - (self.hi - self.lo)}
 
@@ -248,19 +279,25 @@ class PowerIteration:
         mine = y_full[self.lo : self.hi]
         if self._send_idx.numel():
             self.ops.gather(mine, self.lo, self._send_idx, self._send_buf)
+        send_buf, recv_buf = self._send_buf, self._recv_buf
+        if self._staged:
+            self._send_host.copy_(self._send_buf)
+            send_buf, recv_buf = self._send_host, self._recv_host
         ops = []
         for p in range(self.world):
             if p == self.rank:
                 continue
             if self._send_counts[p]:
-                ops.append(dist.P2POp(dist.isend, self._send_buf[self._s_off[p]:self._s_off[p + 1]], p,
+                ops.append(dist.P2POp(dist.isend, send_buf[self._s_off[p]:self._s_off[p + 1]], p,
                                       group=self.group))
             if self._recv_counts[p]:
-                ops.append(dist.P2POp(dist.irecv, self._recv_buf[self._r_off[p]:self._r_off[p + 1]], p,
+                ops.append(dist.P2POp(dist.irecv, recv_buf[self._r_off[p]:self._r_off[p + 1]], p,
                                       group=self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if self._staged:
+            self._recv_buf.copy_(self._recv_host)
         if self._recv_idx.numel():
             self.ops.scatter(self._recv_buf, self._recv_idx, y_full)
 
@@ -271,26 +308,36 @@ class PowerIteration:
         groups match pairwise."""
         me = self.rank
         out = self.x_next[self.lo : self.hi]
+        # staged (gloo): each finished span is copied to the host and sent
+        # from there; received spans are uploaded after the last wait
+        buf = self._host if self._staged else self.x_next
         reqs = []
         for k in range(max(len(sp) for sp in self._spans)):
             mine = self._spans[me][k] if k < len(self._spans[me]) else None
             if mine is not None:
                 self.local_spmv_range(k, self.x, out, self.scale)
+                if self._staged and mine[1] > mine[0]:
+                    buf[mine[0]:mine[1]].copy_(self.x_next[mine[0]:mine[1]])
             ops = []
             for p in range(self.world):
                 if p == me:
                     continue
                 if mine is not None and mine[1] > mine[0]:
-                    ops.append(dist.P2POp(dist.isend, self.x_next[mine[0]:mine[1]], p, group=self.group))
+                    ops.append(dist.P2POp(dist.isend, buf[mine[0]:mine[1]], p, group=self.group))
                 theirs = self._spans[p][k] if k < len(self._spans[p]) else None
                 if theirs is not None and theirs[1] > theirs[0]:
-                    ops.append(dist.P2POp(dist.irecv, self.x_next[theirs[0]:theirs[1]], p, group=self.group))
+                    ops.append(dist.P2POp(dist.irecv, buf[theirs[0]:theirs[1]], p, group=self.group))
             if ops:
                 reqs.extend(dist.batch_isend_irecv(ops))
         self.ops.sumsq(out, self.sumsq)
-        dist.all_reduce(self.sumsq, group=self.group)
+        self._all_reduce_sumsq()
         for r in reqs:
             r.wait()
+        if self._staged:
+            for p in range(self.world):
+                lo, hi = self.bounds[p], self.bounds[p + 1]
+                if p != me and hi > lo:
+                    self.x_next[lo:hi].copy_(buf[lo:hi])
         self.ops.inv_sqrt(self.sumsq, self.scale)
         self.x, self.x_next = self.x_next, self.x
 
@@ -382,7 +429,7 @@ class PowerIteration:
         self.local_spmv(self.x, out, self.scale)
         self.ops.sumsq(out, self.sumsq)
         if self.world > 1:
-            dist.all_reduce(self.sumsq, group=self.group)
+            self._all_reduce_sumsq()
             if self.exchange == "sparse":
                 self._sparse(self.x_next)
             else:

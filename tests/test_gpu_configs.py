@@ -124,7 +124,10 @@ def test_config_parity(sp, name):
     K, hi, hd, hn, tail = port.to_hyb(row, col, val, n)
     mh = sp.to_hyb(m)
     assert mh.k == K and np.array_equal(h(mh.ell.indices), hi)
+    assert h(mh.ell.data.contiguous()).tobytes() == hd.tobytes()
+    assert np.array_equal(h(mh.ell.row_nnz), hn)
     assert np.array_equal(h(mh.coo_tail.row), tail[0]) and np.array_equal(h(mh.coo_tail.col), tail[1])
+    assert h(mh.coo_tail.data).tobytes() == tail[2].tobytes()
     check_within(sp.spmv("hyb", mh, xd), ref, bound)
 
     f = sp.extract_features(m)
