@@ -38,14 +38,16 @@ import torch  # noqa: E402
 
 METRIC = "fp64 SpMV GFLOP/s (2*nnz/t), power-iteration step incl. all-gather of x"
 WORKLOADS = {
-    "C5": dict(scale=25, edge_factor=16, seed=105, x_seed=205, format="csr5"),
-    "C4": dict(scale=21, edge_factor=10, seed=104, x_seed=204, format="csr5"),
-    # BASELINE configs[0..2] (host-generated triplets, ELL by default; under
-    # 4x L2, so timed step by step after an L2 flush): C3 is the
-    # 100-iteration power-iteration config (27-point stencil)
-    "C3": dict(host="C3", x_seed=203, format="ell"),
-    "C2": dict(host="C2", x_seed=202, format="ell"),
-    "C1": dict(host="C1", x_seed=201, format="ell"),
+    "C5": dict(scale=25, edge_factor=16, seed=105, x_seed=205,
+               desc="R-MAT scale 25 ef 16 (a,b,c,d)=(.57,.19,.19,.05), U(0,1] values (BASELINE configs[4])"),
+    "C4": dict(scale=21, edge_factor=10, seed=104, x_seed=204,
+               desc="R-MAT scale 21 ef 10 (BASELINE configs[3])"),
+    # BASELINE configs[0..2] (host-generated triplets; under 4x L2, so timed
+    # step by step after an L2 flush): C3 is the 100-iteration
+    # power-iteration config (27-point stencil)
+    "C3": dict(host="C3", x_seed=203, desc="27-point stencil 88^3 (BASELINE configs[2])"),
+    "C2": dict(host="C2", x_seed=202, desc="banded n=2^20, 8 per row within +-64 (BASELINE configs[1])"),
+    "C1": dict(host="C1", x_seed=201, desc="5-point Laplacian 512^2 (BASELINE configs[0])"),
 }
 
 
@@ -231,12 +233,160 @@ def event_time(fn, reps: int, warm: int = 3) -> float:
     return s.elapsed_time(e) / 1e3 / reps
 
 
+def variant_label(tag, kw):
+    """Stable name of a (format, parameters) pair, e.g. csr5-w32s16, sell-c32s1024."""
+    if tag == "csr5":
+        return f"csr5-w{kw.get('omega', 4)}s{kw.get('sigma', 16)}"
+    if tag == "sell":
+        return f"sell-c{kw.get('sell_c', 4)}s{kw.get('sell_sigma', 0)}"
+    return tag
+
+
+# C1-C4 (the `configs` block of the default run): every format at the
+# reference's default parameters plus the GPU-tuned ones
+CONFIG_VARIANTS = [
+    ("csr", {}),
+    ("csr5", dict(omega=4, sigma=16)),
+    ("csr5", dict(omega=32, sigma=16)),
+    ("ell", {}),
+    ("sell", dict(sell_c=4, sell_sigma=0)),
+    ("sell", dict(sell_c=32, sell_sigma=1024, max_cells=1 << 34)),
+    ("hyb", {}),
+]
+
+
+def load_traffic() -> dict:
+    """ncu DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum
+    of one `ncu --set full` capture) keyed "<config>/<variant>[-relabel]/n<N>"
+    (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py)."""
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return {k: v for k, v in json.loads(tf.read_text()).items() if not k.startswith("_")}
+    except (OSError, ValueError):
+        return {}
+
+
+def use_relabel(args, w) -> bool:
+    return args.relabel == "on" or (args.relabel == "auto" and "scale" in w)
+
+
+def build_workload(sp, synth, w, dev):
+    """Canonical COO of a workload on `dev` (host-generated C1-C3, GPU R-MAT C4/C5)."""
+    if "host" in w:
+        return synth.host_coo(w["host"], device=dev)
+    return synth.rmat_coo(w["scale"], w["edge_factor"], w["seed"], device=dev)
+
+
+def run_configs(args, dev, peak, traffic):
+    """Per-format SpMV of BASELINE configs C1-C4 on this GPU, each rep after
+    an L2 flush (512 MB read), median of `--config-reps`; every result is
+    checked against the sequential oracle on the device (within_tol: |y -
+    y_seq| <= 1e-12 (|A||x|)).  C4 adds CSR5 on the degree-ordered shadow
+    layout (relabel.py); C3 adds its 100-iteration power iteration replayed
+    from a CUDA graph (flushed once before the 100 steps) and run eagerly."""
+    import paper_1805_11938_b200 as sp
+    from paper_1805_11938_b200 import dist as spdist, synth
+    from paper_1805_11938_b200.harness import spmv_bytes
+    from paper_1805_11938_b200.relabel import RelabelledMatrix
+
+    flush = torch.empty(1 << 26, dtype=torch.float64, device=dev)
+    out = {}
+    for name in ("C1", "C2", "C3", "C4"):
+        w = WORKLOADS[name]
+        t_gen = time.perf_counter()
+        a = build_workload(sp, synth, w, dev)
+        torch.cuda.synchronize()
+        t_gen = time.perf_counter() - t_gen
+        n, nnz = a.n_rows, a.nnz
+        x = synth.uniform_vector(n, w["x_seed"], device=dev)
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        ref = sp.dense_spmv_oracle(a, x)
+        bound = sp.dense_spmv_oracle(sp.CooMatrix(n, n, a.row, a.col, a.data.abs()), x.abs())
+        csr = sp.to_csr(a)
+        del a
+        recs = {}
+
+        def measure(label, fn, m_bytes, yv, convert_ms):
+            t = flushed_time(fn, flush, reps=args.config_reps)
+            ok = bool(((yv - ref).abs() <= 1e-12 * bound).all().item())
+            recs[label] = {"us": t * 1e6, "gflops": 2.0 * nnz / t / 1e9, "gbs_model": m_bytes / t / 1e9,
+                           "frac": m_bytes / t / 1e9 / peak, "bytes_model": m_bytes, "convert_ms": convert_ms,
+                           "within_tol": ok, "traffic": traffic.get(f"{name}/{label}/n1")}
+
+        for tag, kw in CONFIG_VARIANTS:
+            label = variant_label(tag, kw)
+            try:
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                m = sp.convert(tag, csr, **kw)
+                if tag in ("csr", "hyb"):
+                    m.chunk_plan()
+                torch.cuda.synchronize()
+                conv = (time.perf_counter() - t0) * 1e3
+            except sp.ConversionError as exc:
+                recs[label] = {"error": f"ConversionError: {str(exc)[:100]}"}
+                continue
+            measure(label, lambda: sp.spmv(tag, m, x, out=y), spmv_bytes(tag, m), y, conv)
+            del m
+        if "scale" in w:  # R-MAT: CSR5 on the degree-ordered shadow layout
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rm = RelabelledMatrix("csr5", csr, omega=32, sigma=16)
+            torch.cuda.synchronize()
+            conv = (time.perf_counter() - t0) * 1e3
+            xp = rm.order.to_new(x)
+            yp = torch.empty_like(xp)
+            fn = lambda: rm.spmv(xp, out=yp)  # noqa: E731
+            fn()
+            measure("csr5-w32s16-relabel", fn, spmv_bytes("csr5", rm.inner), rm.order.to_old(yp), conv)
+            del rm, xp, yp
+        good = {k: v for k, v in recs.items() if "error" not in v}
+        best = max(good, key=lambda k: good[k]["gflops"])
+        entry = {"workload": w["desc"], "n": n, "nnz": nnz, "generate_s": t_gen, "best": best,
+                 "best_gflops": good[best]["gflops"], "best_frac": good[best]["frac"],
+                 "all_within_tol": all(v["within_tol"] for v in good.values()),
+                 "formats": recs}
+        if name == "C3":
+            entry["power_iteration_100"] = c3_power_iteration(sp, spdist, csr, x, flush, nnz)
+        out[name] = entry
+        del csr, x, y, ref, bound
+        torch.cuda.empty_cache()
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def c3_power_iteration(sp, spdist, csr, x0, flush, nnz):
+    """BASELINE configs[2]: 100 iterations x <- A x / ||A x|| (ELL, the best
+    C3 format), L2 flushed once before the 100 steps, timed with CUDA events:
+    replayed from a CUDA graph (PowerIteration.run(graph=True)) and eager."""
+    m = sp.to_ell(csr)
+    res = {"format": "ell", "steps": 100}
+    for mode in ("graph", "eager"):
+        pi = spdist.PowerIteration(lambda xv, o, s: sp.spmv("ell", m, xv, out=o, scale=s), [0, csr.n_rows], 0, 1,
+                                   x0.device, x0)
+        pi.run(4, graph=mode == "graph")  # capture (graph) / warm-up
+        flush.sum()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pi.run(100, graph=mode == "graph")
+        b.record()
+        b.synchronize()
+        t = a.elapsed_time(b) / 1e3
+        res[f"{mode}_us_per_step"] = t / 100 * 1e6
+        res[f"{mode}_gflops"] = 2.0 * nnz * 100 / t / 1e9
+        res[f"{mode}_eigenvalue_estimate"] = pi.eigenvalue_estimate()
+        del pi
+    return res
+
+
 def run_ours(args):
     import torch.distributed as dist
 
     import paper_1805_11938_b200 as sp
     from paper_1805_11938_b200 import _lib, dist as spdist, synth
     from paper_1805_11938_b200.harness import spmv_bytes
+    from paper_1805_11938_b200.relabel import DegreeOrder
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -254,6 +404,9 @@ def run_ours(args):
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
     w = WORKLOADS[args.workload]
     warmup = max(args.warmup, 3)
+    relabel = use_relabel(args, w)
+    peak, peak_src = measured_peak()
+    traffic_db = load_traffic()
 
     # ---- build the matrix (untimed setup; conversion times are reported) ----
     t0 = time.perf_counter()
@@ -288,24 +441,23 @@ def run_ours(args):
     t_csr = time.perf_counter() - t0
     nnz = csr_full.nnz
     del a
-    bounds = (spdist.cost_balanced_bounds(csr_full.ptr, world) if args.balance == "cost"
-              else spdist.nnz_balanced_bounds(csr_full.ptr, world))
-    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    shard = spdist.row_block(csr_full, lo, hi) if world > 1 else csr_full
-    if world > 1:
-        del csr_full
     x_full = synth.uniform_vector(n, w["x_seed"], device=dev)
+    bounds_orig = (spdist.cost_balanced_bounds(csr_full.ptr, world) if args.balance == "cost"
+                   else spdist.nnz_balanced_bounds(csr_full.ptr, world))
+    lo, hi = int(bounds_orig[rank]), int(bounds_orig[rank + 1])
+    shard = spdist.row_block(csr_full, lo, hi) if world > 1 else csr_full
     torch.cuda.empty_cache()
 
-    # ---- per-format candidates on this shard ----
+    # ---- every format on this shard in the reference's layout ----
     formats = {}
     best = None
-    wanted = [f.strip() for f in (args.formats or w["format"]).split(",") if f.strip()]
+    wanted = [f.strip() for f in (args.formats or "csr,csr5,hyb,sell,ell").split(",") if f.strip()]
     y_tmp = torch.empty(shard.n_rows, dtype=torch.float64, device=dev)
     for tag, kw in CANDIDATES:
         if tag not in wanted:
             continue
-        rec = {"params": {k: v for k, v in kw.items() if k != "max_cells"}}
+        label = variant_label(tag, kw)
+        rec = {"format": tag, "params": {k: v for k, v in kw.items() if k != "max_cells"}}
         try:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -316,32 +468,61 @@ def run_ours(args):
             rec["convert_ms"] = (time.perf_counter() - t0) * 1e3
         except (sp.ConversionError, MemoryError, RuntimeError) as exc:
             rec["error"] = f"{type(exc).__name__}: {str(exc)[:120]}"
-            formats[tag] = rec
+            formats[label] = rec
             torch.cuda.empty_cache()
             continue
         t = event_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), reps=args.kernel_reps)
         b = spmv_bytes(tag, m)
-        rec.update(ms=t * 1e3, gflops=2.0 * m.nnz / t / 1e9, gbs_model=b / t / 1e9, bytes_model=b)
-        formats[tag] = rec
-        if best is None or t < best[2]:
-            if best is not None:
-                del best
-            best = (tag, m, t)
+        rec.update(ms=t * 1e3, gflops=2.0 * m.nnz / t / 1e9, gbs_model=b / t / 1e9, bytes_model=b,
+                   frac=b / t / 1e9 / peak, traffic=traffic_db.get(f"{args.workload}/{label}/n{world}"))
+        formats[label] = rec
+        if best is None or t < best[3]:
+            best = (tag, kw, m, t)
         else:
             del m
         torch.cuda.empty_cache()
     if best is None:
         raise RuntimeError("no format converted")
-    tag, m, t_kernel = best
+    tag, kw, m_orig, t_orig = best
     # all ranks must agree on one format: take rank 0's choice
     if world > 1:
-        choice = torch.tensor([[c for c, _ in CANDIDATES].index(tag)], device=dev)
+        names = [variant_label(t_, k_) for t_, k_ in CANDIDATES]
+        choice = torch.tensor([names.index(variant_label(tag, kw))], device=dev)
         dist.broadcast(choice, 0)
-        want = [c for c, _ in CANDIDATES][int(choice.item())]
-        if want != tag:
-            tag = want
-            m = sp.convert(tag, shard, **dict(CANDIDATES)[tag])
-            t_kernel = event_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), reps=args.kernel_reps)
+        want_tag, want_kw = CANDIDATES[int(choice.item())]
+        if variant_label(want_tag, want_kw) != variant_label(tag, kw):
+            tag, kw = want_tag, want_kw
+            m_orig = sp.convert(tag, shard, **kw)
+    label = variant_label(tag, kw)
+
+    # ---- the layout the power iteration runs on ----
+    # R-MAT: the degree-ordered shadow copy P A P^T (relabel.py), iterating
+    # on x' = P x; the reference-layout matrix m_orig stays for the e2e calls
+    t_relabel = None
+    if relabel:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        order = DegreeOrder(csr_full)
+        csr_run = order.matrix(csr_full)
+        bounds = (spdist.cost_balanced_bounds(csr_run.ptr, world) if args.balance == "cost"
+                  else spdist.nnz_balanced_bounds(csr_run.ptr, world))
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        shard_run = spdist.row_block(csr_run, lo, hi) if world > 1 else csr_run
+        m = sp.convert(tag, shard_run, **kw)
+        if tag in ("csr", "hyb"):
+            m.chunk_plan()
+        x_run = order.to_new(x_full)
+        torch.cuda.synchronize()
+        t_relabel = time.perf_counter() - t0
+        if world > 1:
+            del csr_run
+        del order
+    else:
+        bounds, shard_run, m, x_run = bounds_orig, shard, m_orig, x_full
+    if world > 1:
+        del csr_full
+    torch.cuda.empty_cache()
+    t_kernel = event_time(lambda: sp.spmv(tag, m, x_run, out=y_tmp), reps=args.kernel_reps)
 
     # a shard whose format bytes are under 4x L2 would be partly served from
     # L2 by back-to-back steps: time the kernel and every step after an L2
@@ -349,19 +530,13 @@ def run_ours(args):
     flush = None
     if spmv_bytes(tag, m) < 4 * 126e6:
         flush = torch.empty(1 << 26, dtype=torch.float64, device=dev)
-        t_kernel = flushed_time(lambda: sp.spmv(tag, m, x_full, out=y_tmp), flush, reps=args.kernel_reps)
+        t_kernel = flushed_time(lambda: sp.spmv(tag, m, x_run, out=y_tmp), flush, reps=args.kernel_reps)
 
     # ---- roofline of the dominant kernel (this rank's shard) ----
-    peak, peak_src = measured_peak()
+    run_label = label + ("-relabel" if relabel else "")
     bytes_model = spmv_bytes(tag, m)
     achieved = bytes_model / t_kernel / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get(f"{args.workload}/{tag}/n{world}")
-        except ValueError:
-            traffic = None
+    traffic = traffic_db.get(f"{args.workload}/{run_label}/n{world}")
     # Gather ceiling, measured live: on power-law matrices the SpMV is bound by
     # the L1TEX rate of its random x gathers, not by HBM.  spmvb_gather_probe
     # sums x at this shard's own column indices (all of them, same x, no
@@ -370,13 +545,14 @@ def run_ours(args):
     stream_ptr = torch.cuda.current_stream(dev).cuda_stream
 
     def probe():
-        _lib.check(_lib.load().spmvb_gather_probe(x_full.data_ptr(), shard.indices.data_ptr(), shard.nnz,
+        _lib.check(_lib.load().spmvb_gather_probe(x_run.data_ptr(), shard_run.indices.data_ptr(), shard_run.nnz,
                                                   gpart.data_ptr(), stream_ptr))
 
     t_gather = event_time(probe, reps=10)
     del gpart
     gather = {"gathers_per_launch": int(m.nnz), "achieved_G_per_s": m.nnz / t_kernel / 1e9,
-              "peak_G_per_s": shard.nnz / t_gather / 1e9, "frac": (m.nnz / t_kernel) / (shard.nnz / t_gather),
+              "peak_G_per_s": shard_run.nnz / t_gather / 1e9,
+              "frac": (m.nnz / t_kernel) / (shard_run.nnz / t_gather),
               "peak_source": "spmvb_gather_probe: x summed at all of this shard's column indices (CUDA events)"}
 
     # ---- timed power iteration ----
@@ -391,12 +567,12 @@ def run_ours(args):
         k_all = len(tb) - 1
         plan = [(int(rb[k]), int(rb[k + 1]) if k + 1 < k_all else m.n_rows, int(tb[k]), int(tb[k + 1]))
                 for k in range(k_all)][::-1]
-        ranges = [(a, b) for a, b, _, _ in plan]
+        ranges = [(a_, b_) for a_, b_, _, _ in plan]
         carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=dev)
 
         def range_fn(k, xv, out, scale):
-            a, b, t0, t1 = plan[k]
-            sp.spmv_csr5_tiles(m, xv, out, t0, t1, a, b, scale=scale, carry=carry)
+            a_, b_, t0_, t1_ = plan[k]
+            sp.spmv_csr5_tiles(m, xv, out, t0_, t1_, a_, b_, scale=scale, carry=carry)
 
     # p2p exchange with CSR5 omega=32 shards: the SpMV kernel itself stores
     # each block's rows into the peers' next iterate (one fused kernel)
@@ -408,8 +584,8 @@ def run_ours(args):
             sp.spmv_csr5_push(m, xv, out, peers, off, scale=scale, carry=carry_p)
 
     def make_pi(exchange):
-        return spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_full, exchange=exchange,
-                                     local_cols=shard.indices if exchange == "sparse" else None,
+        return spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_run, exchange=exchange,
+                                     local_cols=shard_run.indices if exchange == "sparse" else None,
                                      local_ranges=ranges if exchange in ("allgatherv", "p2p") else None,
                                      local_spmv_range=range_fn,
                                      local_spmv_push=push_fn if exchange == "p2p" else None)
@@ -447,13 +623,13 @@ def run_ours(args):
             flush.sum()
             if world > 1:
                 dist.barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record()
             pi.step()
-            b.record()
-            evs.append((a, b))
+            b_.record()
+            evs.append((a_, b_))
         torch.cuda.synchronize()
-        t_loop = sum(a.elapsed_time(b) for a, b in evs) / 1e3
+        t_loop = sum(a_.elapsed_time(b_) for a_, b_ in evs) / 1e3
     if world > 1:
         dist.barrier()
     launches = _lib.load().spmvb_launch_count() - launches0  # the flush is a torch kernel, not counted
@@ -463,6 +639,7 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_loop = float(tt.item())
     value = 2.0 * nnz * args.steps / t_loop / 1e9
+    eig = pi.eigenvalue_estimate()
     exchange = {"mode": pi.exchange, "overlap_ranges": len(ranges) if ranges else 1,
                 f"ms_per_step_{pi.exchange}": t_loop / args.steps * 1e3}
     if world > 1:
@@ -495,38 +672,66 @@ def run_ours(args):
                 exchange[f"error_{other}"] = f"{type(exc).__name__}: {str(exc)[:160]}"
         if vol:
             exchange["rank0_volume_entries"] = vol
+    else:
+        del pi
 
     # ---- end to end through the public API with host buffers ----
-    # Every step copies its x in from pinned host memory and its y back to a
-    # caller-owned pinned host buffer.  Headline: spmv_many over the steps'
-    # vectors (step k+1's x is copied in while step k computes and its y is
-    # copied back: both PCIe directions busy); also reported: one synchronous
-    # spmv(..., out=) call per step.
-    x_hosts = [x_full.cpu().pin_memory() for _ in range(2)]
-    y_hosts = [torch.empty(m.n_rows, dtype=torch.float64).pin_memory() for _ in range(2)]
+    # Headline: a dependent chain of single calls on the reference-layout
+    # matrix, each call's output the next call's input (the shape of a
+    # host-vector power iteration): spmv(tag, m, pinned_x, out=pinned_y,
+    # scale=s) copies x in, computes, and copies y back before returning.
+    # Secondary: spmv_many over independent vectors (copies of step k+1
+    # overlap step k: not possible for a dependent chain).
     e2e_steps = max(2, min(args.steps, args.e2e_steps))
-    sp.spmv(tag, m, x_hosts[0], out=y_hosts[0])
-    sp.spmv_many(tag, m, x_hosts, y_hosts)
+    bufs = [x_full.cpu().pin_memory(), torch.empty(m_orig.n_rows, dtype=torch.float64).pin_memory()]
+    chain_ok = m_orig.n_rows == m_orig.n_cols
+    s_dev = torch.ones(1, dtype=torch.float64, device=dev)
+    if chain_ok:
+        y0 = sp.spmv(tag, m_orig, x_full)
+        s_dev.fill_(1.0 / float(torch.linalg.vector_norm(y0).item() or 1.0))  # keeps the chain's magnitudes bounded
+        del y0
     if world > 1:
         dist.barrier()
+    sp.spmv(tag, m_orig, bufs[0], out=bufs[1], scale=s_dev)  # warm-up (pins the host path's buffers)
     t0 = time.perf_counter()
-    sp.spmv_many(tag, m, [x_hosts[k % 2] for k in range(e2e_steps)], [y_hosts[k % 2] for k in range(e2e_steps)])
-    t_e2e = time.perf_counter() - t0
+    for k in range(e2e_steps):
+        if chain_ok:
+            sp.spmv(tag, m_orig, bufs[k % 2], out=bufs[(k + 1) % 2], scale=s_dev)
+        else:
+            sp.spmv(tag, m_orig, bufs[0], out=bufs[1], scale=s_dev)
+    t_chain = time.perf_counter() - t0
+    x_hosts = [x_full.cpu().pin_memory() for _ in range(2)]
+    y_hosts = [torch.empty(m_orig.n_rows, dtype=torch.float64).pin_memory() for _ in range(2)]
+    sp.spmv_many(tag, m_orig, x_hosts, y_hosts)
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        sp.spmv(tag, m, x_hosts[0], out=y_hosts[0])
-    t_single = time.perf_counter() - t0
+    sp.spmv_many(tag, m_orig, [x_hosts[k % 2] for k in range(e2e_steps)], [y_hosts[k % 2] for k in range(e2e_steps)])
+    t_many = time.perf_counter() - t0
     if world > 1:
-        tt = torch.tensor([t_e2e, t_single], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_chain, t_many], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e, t_single = float(tt[0].item()), float(tt[1].item())
-    e2e = {"value": 2.0 * nnz * e2e_steps / t_e2e / 1e9, "unit": "GFLOP/s",
-           "h2d_bytes_per_step": int(x_hosts[0].numel() * 8), "d2h_bytes_per_step": int(y_hosts[0].numel() * 8),
+        t_chain, t_many = float(tt[0].item()), float(tt[1].item())
+    e2e = {"value": 2.0 * nnz * e2e_steps / t_chain / 1e9, "unit": "GFLOP/s",
+           "h2d_bytes_per_step": int(bufs[0].numel() * 8), "d2h_bytes_per_step": int(bufs[1].numel() * 8),
            "steps": e2e_steps,
-           "api": f"paper_1805_11938_b200.spmv_many('{tag}', m, pinned_host_xs, pinned_host_ys) "
-                  "(transfers pipelined across the steps' vectors)",
-           "single_call_value": 2.0 * nnz * e2e_steps / t_single / 1e9,
-           "single_call_api": f"paper_1805_11938_b200.spmv('{tag}', m, pinned_host_x, out=pinned_host_y) per step"}
+           "api": (f"paper_1805_11938_b200.spmv('{tag}', m, pinned_host_x_k, out=pinned_host_x_k+1, scale=s) per "
+                   f"step, x_k+1 = the previous call's output (dependent chain, {variant_label(tag, kw)}, "
+                   "reference layout)" if chain_ok else "single spmv call per step"),
+           "independent_vectors_value": 2.0 * nnz * e2e_steps / t_many / 1e9,
+           "independent_vectors_api": (f"paper_1805_11938_b200.spmv_many('{tag}', m, pinned_host_xs, "
+                                       "pinned_host_ys): transfers of vector k+1 overlap vector k")}
+    del bufs, x_hosts, y_hosts
+
+    # ---- C1-C4 per format (rank 0, N = 1) ----
+    configs = None
+    if rank == 0 and world == 1 and args.workload == "C5" and not args.no_configs:
+        del m_orig, m
+        if relabel:
+            del csr_run
+        del shard, shard_run, x_run
+        if world == 1:
+            del csr_full
+        torch.cuda.empty_cache()
+        configs = run_configs(args, dev, peak, traffic_db)
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
@@ -535,14 +740,14 @@ def run_ours(args):
 
         cores = port.host_cores()
         if "host" in w:
-            ptr, ind, dat, n_s = host_csr(w["host"])
+            ptr_h, ind, dat, n_s = host_csr(w["host"])
             what = f"the whole matrix ({n_s} rows, {int(ind.size)} nnz)"
         else:
-            ptr, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
-                                                                 args.cpu_keep_mod, cores)
+            ptr_h, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
+                                                                   args.cpu_keep_mod, cores)
             what = f"{n_s} rows (1/{args.cpu_keep_mod} hashed row sample), {int(ind.size)} nnz, full x"
         xs = synth_ref.uniform(n, w["x_seed"])
-        tc, reps = cpu_baseline.time_csr(ptr, ind, dat, n_s, xs, cores, min_seconds=args.cpu_seconds)
+        tc, reps = cpu_baseline.time_csr(ptr_h, ind, dat, n_s, xs, cores, min_seconds=args.cpu_seconds)
         cpu = {"value": 2.0 * ind.size / tc / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                "sample": f"{what}; spmvkit spmv_csr algorithm (oracle/port.py), {reps} reps",
                "cpu": cpu_baseline.cpu_model()}
@@ -552,19 +757,24 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": warmup, "ms_per_step": t_loop / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "format": tag, "params": formats[tag]["params"], "n": n,
+            "config": {"workload": args.workload, "desc": w["desc"], "format": tag, "variant": label,
+                       "params": {k: v for k, v in kw.items() if k != "max_cells"}, "n": n,
                        "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
                        "balance": args.balance,
+                       "layout": ("degree-ordered shadow P A P^T (relabel.py), iterate x' = P x; the reference-layout "
+                                  "matrix serves the e2e calls" if relabel else "reference layout"),
                        "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"
                                 if world > 1 else "y=s*A x; ||y||^2; s=1/||y||"),
+                       "eigenvalue_estimate": eig,
                        "l2": (f"inputs larger than L2 ({bytes_model / 1e6:.0f} MB of format bytes per SpMV, "
                               f"> 4 x 126 MB), no flush" if flush is None else
                               f"{bytes_model / 1e6:.0f} MB of format bytes per SpMV (< 4 x 126 MB L2): L2 flushed by a "
                               f"512 MB read before every timed step and kernel rep, each timed on its own")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": f"spmv_{tag} (rank 0 shard)", "bytes_per_launch": bytes_model,
+                         "kernel": f"spmv_{tag} {run_label} (rank 0 shard)", "bytes_per_launch": bytes_model,
                          "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0,
+                         "reference_layout_frac": formats[label]["frac"] if label in formats else None,
                          "gather_bound": gather},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -572,8 +782,9 @@ def run_ours(args):
             "exchange": exchange,
             "clocks": clk,
             "formats": formats,
+            "configs": configs,
             "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "canonicalize_first_call_s": t_canon_first,
-                           "to_csr_s": t_csr,
+                           "to_csr_s": t_csr, "relabel_and_convert_s": t_relabel,
                            "canonicalize_Mentries_per_s": raw_nnz / t_canon / 1e6},
         })
     if world > 1:
@@ -616,11 +827,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
-    # Candidate formats; the fastest drives the timed power iteration.  The
-    # default is the format that won the full sweep (--formats
-    # csr,csr5,hyb,sell,ell; profiles/r01_bench_c5_sweep.json), so the
-    # default command is cheap and stable under ncu's serialised replay.
+    # Formats timed on the workload (reference layout, one record each, as
+    # the reference's run_bench); the fastest drives the timed power
+    # iteration.  Default: all five (ELL raises ConversionError on R-MAT).
     ap.add_argument("--formats", default=None)
+    ap.add_argument("--relabel", choices=["auto", "on", "off"], default="auto",
+                    help="run the power iteration on the degree-ordered shadow layout (auto: R-MAT workloads)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 per-format block of the C5 run")
+    ap.add_argument("--config-reps", type=int, default=10)
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--overlap-ranges", type=int, default=4,
