@@ -157,6 +157,35 @@ def emit(obj):
 # --------------------------------------------------------------------------
 # Reference arm: the reference's CPU algorithm on a bounded sample
 # --------------------------------------------------------------------------
+def cpu_reference_matrix(args, w, cores):
+    """Host CSR the CPU reference runs on: C1-C3 whole (oracle canonicalize);
+    R-MAT whole when the host has the RAM (~40 B per draw at peak;
+    oracle/rmat_sample.c:rmat_csr, int64 indices as the reference's arrays),
+    else the hashed 1/keep_mod row sample with the full-length x.  Returns
+    (ptr, indices, data, n_rows, description, build seconds)."""
+    from oracle import cpu_baseline
+
+    t0 = time.perf_counter()
+    if "host" in w:
+        ptr, ind, dat, n_s = host_csr(w["host"])
+        return ptr, ind, dat, n_s, f"the whole {args.workload} matrix ({n_s} rows, {int(ind.size)} nnz)", \
+            time.perf_counter() - t0
+    draws = w["edge_factor"] << w["scale"]
+    need = 40 * draws
+    full = args.cpu_sample == "full" or (args.cpu_sample == "auto" and cpu_baseline.host_ram_available() >= 2 * need)
+    if full:
+        ptr, ind, dat = cpu_baseline.rmat_full_csr(w["scale"], w["edge_factor"], w["seed"], cores)
+        n_s = ptr.size - 1
+        what = f"the whole {args.workload} matrix ({n_s} rows, {int(ind.size)} nnz)"
+    else:
+        ptr, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
+                                                             args.cpu_keep_mod, cores)
+        what = (f"{n_s} rows of {args.workload} (hashed 1/{args.cpu_keep_mod} row sample: the host has "
+                f"{cpu_baseline.host_ram_available() / 1e9:.0f} GB available, the whole matrix needs "
+                f"~{2 * need / 1e9:.0f}), {int(ind.size)} nnz, full-length x")
+    return ptr, ind, dat, n_s, what, time.perf_counter() - t0
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -165,12 +194,8 @@ def run_reference(args):
 
     w = WORKLOADS[args.workload]
     cores = port.host_cores()
-    if "host" in w:  # the whole matrix
-        ptr, ind, dat, n = host_csr(w["host"])
-        n_s = n
-    else:
-        ptr, ind, dat, n_s, n = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
-                                                             args.cpu_keep_mod, cores)
+    ptr, ind, dat, n_s, what, t_build = cpu_reference_matrix(args, w, cores)
+    n = 1 << w["scale"] if "scale" in w else n_s
     x = synth_ref.uniform(n, w["x_seed"])
     nnz_s = int(ind.size)
     for _ in range(max(args.warmup, 1)):
@@ -182,17 +207,13 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
     gflops = 2.0 * nnz_s / t / 1e9
-    sample = (f"rows with mix64(r^0xA5A5A5A5) % {args.cpu_keep_mod} == 0 of {args.workload}: {n_s} rows, "
-              f"{nnz_s} nnz, full-length x ({n}); spmvkit.kernels.spmv_csr algorithm (oracle/port.py), "
-              f"workers={cores}") if "host" not in w else (
-              f"the whole {args.workload} matrix ({n} rows, {nnz_s} nnz); spmvkit.kernels.spmv_csr algorithm "
-              f"(oracle/port.py), workers={cores}")
+    sample = f"{what}; spmvkit.kernels.spmv_csr algorithm (oracle/port.py), workers={cores}, one SpMV per step"
     emit({
         "impl": "reference", "metric": METRIC, "value": gflops, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "format": "csr", "n": n, "sample_nnz": nnz_s,
-                   "parallelism": f"cpu threads x{cores}"},
+        "config": {"workload": args.workload, "desc": w["desc"], "format": "csr", "n": n, "sample_nnz": nnz_s,
+                   "parallelism": f"cpu threads x{cores}", "host_build_s": t_build},
         "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample,
                          "cpu": cpu_baseline.cpu_model()},
         "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -363,8 +384,7 @@ def c3_power_iteration(sp, spdist, csr, x0, flush, nnz):
     m = sp.to_ell(csr)
     res = {"format": "ell", "steps": 100}
     for mode in ("graph", "eager"):
-        pi = spdist.PowerIteration(lambda xv, o, s: sp.spmv("ell", m, xv, out=o, scale=s), [0, csr.n_rows], 0, 1,
-                                   x0.device, x0)
+        pi = spdist.PowerIteration(sp.SpmvOperator("ell", m), [0, csr.n_rows], 0, 1, x0.device, x0)
         pi.run(4, graph=mode == "graph")  # capture (graph) / warm-up
         flush.sum()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -556,8 +576,8 @@ def run_ours(args):
               "peak_source": "spmvb_gather_probe: x summed at all of this shard's column indices (CUDA events)"}
 
     # ---- timed power iteration ----
-    def local_spmv(xv, out, scale):
-        sp.spmv(tag, m, xv, out=out, scale=scale)
+    # (a single process binds its launches once per buffer parity: dist.PowerIteration fast path)
+    local_spmv = sp.SpmvOperator(tag, m)
 
     # overlap (N > 1, CSR5 shards): row-aligned tile ranges, light rows first,
     # each range's rows sent to the peers while the next range computes
@@ -739,18 +759,13 @@ def run_ours(args):
         from oracle import cpu_baseline, port, synth_ref
 
         cores = port.host_cores()
-        if "host" in w:
-            ptr_h, ind, dat, n_s = host_csr(w["host"])
-            what = f"the whole matrix ({n_s} rows, {int(ind.size)} nnz)"
-        else:
-            ptr_h, ind, dat, n_s, _ = cpu_baseline.rmat_row_sample(w["scale"], w["edge_factor"], w["seed"],
-                                                                   args.cpu_keep_mod, cores)
-            what = f"{n_s} rows (1/{args.cpu_keep_mod} hashed row sample), {int(ind.size)} nnz, full x"
+        ptr_h, ind, dat, n_s, what, t_build = cpu_reference_matrix(args, w, cores)
         xs = synth_ref.uniform(n, w["x_seed"])
         tc, reps = cpu_baseline.time_csr(ptr_h, ind, dat, n_s, xs, cores, min_seconds=args.cpu_seconds)
         cpu = {"value": 2.0 * ind.size / tc / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                "sample": f"{what}; spmvkit spmv_csr algorithm (oracle/port.py), {reps} reps",
-               "cpu": cpu_baseline.cpu_model()}
+               "cpu": cpu_baseline.cpu_model(), "host_build_s": t_build}
+        del ptr_h, ind, dat
 
     if rank == 0:
         emit({
@@ -849,6 +864,8 @@ def main():
     ap.add_argument("--p2p-unfused", action="store_true",
                     help="p2p exchange with a separate push kernel per row range instead of the fused SpMV+push")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)
+    ap.add_argument("--cpu-sample", choices=["auto", "full", "rows"], default="auto",
+                    help="CPU reference on R-MAT: the whole matrix (auto: when the host RAM allows) or a row sample")
     ap.add_argument("--cpu-keep-mod", type=int, default=64)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -297,6 +297,13 @@ int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int6
 int spmvb_sumsq(const double* y, int64_t n, double* out, void* stream);
 /* scale_out = 1/sqrt(*sumsq) (device scalars). */
 int spmvb_inv_sqrt(const double* sumsq, double* scale_out, void* stream);
+/* Both in one launch: *sumsq = ||y||^2, *scale_out = 1/||y|| (1 if y == 0),
+ * deterministic (block partials folded in block order).  ws: a device
+ * buffer of spmvb_norm_ws_bytes() bytes, zeroed once when allocated, used by
+ * one stream at a time (the kernel leaves it ready for the next call).  The
+ * normalisation of a single-process power-iteration step. */
+int64_t spmvb_norm_ws_bytes(void);
+int spmvb_norm_scale(const double* y, int64_t n, void* ws, double* sumsq, double* scale_out, void* stream);
 
 /* Sparse x exchange of the row-block power iteration (a shard
  * reads only ~20% of the columns at C4/C5, so receiving just those entries

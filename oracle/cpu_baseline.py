@@ -38,7 +38,46 @@ def _lib():
                                        ctypes.c_double, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p,
                                        ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    lib.rmat_csr.restype = ctypes.c_int64
+    lib.rmat_csr.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                             ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                             ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
+    lib.rmat_csr_free.restype = None
+    lib.rmat_csr_free.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     return lib
+
+
+def rmat_full_csr(scale: int, edge_factor: int, seed: int, threads: int | None = None):
+    """The whole R-MAT matrix (first-draw dedup) as canonical host CSR
+    (ptr, indices, data) with int64 indices like the reference's arrays
+    (formats.py:183-188), built by oracle/rmat_sample.c:rmat_csr."""
+    threads = threads or port.host_cores()
+    lib = _lib()
+    n = 1 << scale
+    p, c, v = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    nnz = lib.rmat_csr(scale, edge_factor << scale, 0.57, 0.19, 0.19, seed, threads, ctypes.byref(p),
+                       ctypes.byref(c), ctypes.byref(v))
+    if nnz < 0:
+        raise MemoryError("rmat_csr: host allocation failed")
+    try:
+        ptr = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_int64)), (n + 1,)).copy()
+        ind = np.ctypeslib.as_array(ctypes.cast(c, ctypes.POINTER(ctypes.c_int32)), (max(nnz, 1),))[:nnz]
+        ind = ind.astype(np.int64)
+        dat = np.ctypeslib.as_array(ctypes.cast(v, ctypes.POINTER(ctypes.c_double)), (max(nnz, 1),))[:nnz].copy()
+    finally:
+        lib.rmat_csr_free(p, c, v)
+    return ptr, ind, dat
+
+
+def host_ram_available() -> int:
+    """MemAvailable of this host in bytes (0 if unknown)."""
+    try:
+        for line in Path("/proc/meminfo").read_text().splitlines():
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except (OSError, ValueError, IndexError):
+        pass
+    return 0
 
 
 def kept_rows(n: int, keep_mod: int) -> np.ndarray:

@@ -296,6 +296,47 @@ __global__ void k_inv_sqrt(const double* sumsq, double* scale) {
   *scale = (s > 0.0) ? 1.0 / sqrt(s) : 1.0;
 }
 
+// ||y||^2 and 1/||y|| in ONE launch (the normalisation of a single-process
+// power-iteration step): each block writes its partial sum, the last block
+// to take a ticket folds the partials in block order and resets the ticket.
+// The grid depends on n only, so the result is the same on every call.
+constexpr int NORM_THREADS = 256;
+constexpr int NORM_MAX_BLOCKS = 148 * 8;
+struct NormWs {
+  double part[NORM_MAX_BLOCKS];
+  unsigned ticket;
+};
+
+__global__ void __launch_bounds__(NORM_THREADS) k_norm_scale(const double* __restrict__ y, int64_t n, NormWs* ws,
+                                                             double* __restrict__ sumsq, double* __restrict__ scale) {
+  __shared__ double tmp[NORM_THREADS / 32];
+  __shared__ bool last;
+  pdl_wait();
+  double acc = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * NORM_THREADS;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(NORM_THREADS) + threadIdx.x; i < n; i += stride) {
+    const double v = y[i];
+    acc = fma(v, v, acc);
+  }
+  acc = block_reduce<double, NORM_THREADS>(acc, OpSum{}, 0.0, tmp);
+  if (threadIdx.x == 0) {
+    ws->part[blockIdx.x] = acc;
+    __threadfence();
+    last = atomicAdd(&ws->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += NORM_THREADS) s += __ldcg(ws->part + b);
+  s = block_reduce<double, NORM_THREADS>(s, OpSum{}, 0.0, tmp);
+  if (threadIdx.x == 0) {
+    *sumsq = s;
+    *scale = (s > 0.0) ? 1.0 / sqrt(s) : 1.0;
+    ws->ticket = 0;
+  }
+}
+
 void check_shape(int64_t n_rows, int64_t n_cols) {
   if (n_rows < 0 || n_cols < 0) fail(SPMVB_INVALID_ARG, "negative matrix shape %lldx%lld", (long long)n_rows, (long long)n_cols);
   if (n_rows > INT32_MAX || n_cols > INT32_MAX)
@@ -549,6 +590,21 @@ extern "C" int spmvb_sumsq(const double* y, int64_t n, double* out, void* stream
     cudaStream_t s = as_stream(stream);
     device_reduce<double>(
         n, [=] __device__(int64_t i) { double v = y[i]; return v * v; }, OpSum{}, 0.0, out, s, /*pdl=*/true);
+  });
+}
+
+extern "C" int64_t spmvb_norm_ws_bytes(void) { return static_cast<int64_t>(sizeof(NormWs)); }
+
+extern "C" int spmvb_norm_scale(const double* y, int64_t n, void* ws, double* sumsq, double* scale_out,
+                                void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    if (!ws || !sumsq || !scale_out) fail(SPMVB_INVALID_ARG, "ws, sumsq and scale_out are required");
+    if (n < 0) fail(SPMVB_INVALID_ARG, "negative length %lld", (long long)n);
+    const unsigned blocks = grid_for(n, NORM_THREADS * 8, NORM_MAX_BLOCKS);
+    launch_pdl(k_norm_scale, dim3(blocks), dim3(NORM_THREADS), 0, s, y, n, static_cast<NormWs*>(ws), sumsq,
+               scale_out);
+    SPMVB_LAUNCHED("k_norm_scale");
   });
 }
 

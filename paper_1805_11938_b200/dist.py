@@ -103,6 +103,16 @@ class GpuOps:
             check(LIB.spmvb_inv_sqrt(ptr(sumsq), ptr(scale), _lib.stream(sumsq.device)))
 
     @staticmethod
+    def bind_norm_scale(y: torch.Tensor, sumsq: torch.Tensor, scale: torch.Tensor):
+        """A prepared ``sumsq = ||y||^2; scale = 1/||y||`` (one launch,
+        spmvb_norm_scale) on these buffers, with its own workspace."""
+        from .kernels import BoundCall
+
+        ws = torch.zeros(int(LIB.spmvb_norm_ws_bytes()), dtype=torch.uint8, device=y.device)
+        return BoundCall("spmvb_norm_scale", (ptr(y), y.numel(), ptr(ws), ptr(sumsq), ptr(scale)),
+                         _lib.stream(y.device), keep=(y, sumsq, scale, ws))
+
+    @staticmethod
     def column_set(cols: torch.Tensor, n_cols: int) -> torch.Tensor:
         """Sorted distinct column ids (int32) of ``cols``."""
         dev = cols.device
@@ -184,6 +194,12 @@ class PowerIteration:
             if local_cols is None:
                 raise ValueError("exchange='sparse' needs local_cols (the shard's column indices)")
             self._plan_sparse(local_cols, n)
+        # prepared launches (single process, plain exchange, a local_spmv that
+        # can bind, the library's ops): per x/x_next parity the SpMV and the
+        # fused norm are bound once, so a step is two ctypes calls
+        self._fast = None
+        self._fast_ok = (world == 1 and self.exchange == "allgatherv" and device.type == "cuda"
+                         and hasattr(local_spmv, "bind") and self.ops is GpuOps)
         self._spans = None
         if local_ranges is not None and world > 1 and self.exchange == "allgatherv":
             if local_spmv_range is None:
@@ -418,7 +434,27 @@ class PowerIteration:
         self._cur = nxt
         self.x, self.x_next = self.x_next, self.x
 
+    def _fast_calls(self):
+        """The bound (SpMV, norm) launches for the current x/x_next buffers
+        and stream, bound on first use (at most a few sets are kept)."""
+        key = (self.x.data_ptr(), self.x_next.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        f = self._fast
+        if f is None or len(f) >= 4 and key not in f:
+            f = self._fast = {}
+        calls = f.get(key)
+        if calls is None:
+            out = self.x_next[self.lo : self.hi]
+            calls = f[key] = (self.local_spmv.bind(self.x, out, self.scale),
+                              GpuOps.bind_norm_scale(out, self.sumsq, self.scale))
+        return calls
+
     def step(self) -> None:
+        if self._fast_ok:
+            spmv_call, norm_call = self._fast_calls()
+            spmv_call()
+            norm_call()
+            self.x, self.x_next = self.x_next, self.x
+            return
         if self.exchange == "p2p":
             self._step_p2p()
             return

@@ -25,7 +25,7 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import Csr5Matrix, CsrMatrix, EllMatrix, FormatMatrix, FormatTag, HybMatrix, SellMatrix
 
-__all__ = ["plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push", "spmv_csr5_tiles", "spmv_ell",
+__all__ = ["BoundCall", "SpmvOperator", "bind", "plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push", "spmv_csr5_tiles", "spmv_ell",
            "spmv_hyb", "spmv_many", "spmv_sell"]
 
 
@@ -112,18 +112,24 @@ def _run(m, x, out, scale, launch):
     return _finish_y(y, how)
 
 
+def _args_csr(m: CsrMatrix, xd, y, sp, scratch):
+    plan = m.chunk_plan()
+    cr, cv = scratch
+    return "spmvb_spmv_csr", (m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.nz_rows), plan.n_nz,
+                              ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp)
+
+
+def _scratch_csr(m: CsrMatrix):
+    return m.chunk_plan().scratch(m.device)
+
+
 def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None):
     """y = A x for CSR via the chunked kernel (kernels.py:76-95)."""
-    plan = m.chunk_plan()
+    m.chunk_plan()
 
     def launch(xd, y, sp, s):
-        cr, cv = plan.scratch(m.device)
-        check(
-            LIB.spmvb_spmv_csr(
-                m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(plan.nz_rows), plan.n_nz,
-                ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y), sp, s,
-            )
-        )
+        name, args = _args_csr(m, xd, y, sp, _scratch_csr(m))
+        check(getattr(LIB, name)(*args, s))
 
     return _run(m, x, out, scale, launch)
 
@@ -138,6 +144,16 @@ def _packed_flags(m: Csr5Matrix):
     return m.flag_bits if m.n_cols * 8 >= _PACKED_FLAGS_MIN_X_BYTES else None
 
 
+def _args_csr5(m: Csr5Matrix, xd, y, sp, carry):
+    return "spmvb_spmv_csr5", (m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag),
+                               ptr(_packed_flags(m)), ptr(m.indices), ptr(m.data), ptr(m.tile_aux),
+                               ptr(m.nonempty_rows), m.n_nonempty, ptr(carry), ptr(xd), ptr(y), sp)
+
+
+def _scratch_csr5(m: Csr5Matrix):
+    return torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
+
+
 def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None, ranges: int = 16):
     """y = A x for CSR5: per-tile segmented sums + ordered carry fix-up (kernels.py:139-174).
 
@@ -149,15 +165,8 @@ def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None, range
         return _spmv_csr5_host(m, x, out, scale, ranges)
 
     def launch(xd, y, sp, s):
-        carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
-        check(
-            LIB.spmvb_spmv_csr5(
-                m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag),
-                ptr(_packed_flags(m)), ptr(m.indices),
-                ptr(m.data),
-                ptr(m.tile_aux), ptr(m.nonempty_rows), m.n_nonempty, ptr(carry), ptr(xd), ptr(y), sp, s,
-            )
-        )
+        name, args = _args_csr5(m, xd, y, sp, _scratch_csr5(m))
+        check(getattr(LIB, name)(*args, s))
 
     return _run(m, x, out, scale, launch)
 
@@ -251,46 +260,59 @@ def _spmv_csr5_host(m: Csr5Matrix, x, out, scale, ranges: int):
     return yh if kind == "tensor" else yh.numpy()
 
 
+def _args_ell(m: EllMatrix, xd, y, sp, scratch):
+    return "spmvb_spmv_ell", (m.n_rows, m.k, ptr(m.grid_indices), ptr(m.grid_data), ptr(xd), ptr(y), sp)
+
+
 def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
     """y = A x for ELL, sequential over the k slots (kernels.py:98-116)."""
 
     def launch(xd, y, sp, s):
-        check(LIB.spmvb_spmv_ell(m.n_rows, m.k, ptr(m.grid_indices), ptr(m.grid_data), ptr(xd), ptr(y), sp, s))
+        name, args = _args_ell(m, xd, y, sp, None)
+        check(getattr(LIB, name)(*args, s))
 
     return _run(m, x, out, scale, launch)
+
+
+def _args_sell(m: SellMatrix, xd, y, sp, scratch):
+    wide, n_wide, max_narrow, first_piece, n_pieces = m.wide_plan()
+    perm = m.perm if m.sigma > 0 else None
+    return "spmvb_spmv_sell", (m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices),
+                               ptr(m.flat_data), ptr(wide), n_wide, ptr(first_piece), n_pieces, max_narrow, ptr(xd),
+                               ptr(y), sp)
 
 
 def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
     """y = A x for SELL / SELL-C-sigma, scattered through perm (kernels.py:119-136)."""
-
-    wide, n_wide, max_narrow, first_piece, n_pieces = m.wide_plan()
+    m.wide_plan()
 
     def launch(xd, y, sp, s):
-        perm = m.perm if m.sigma > 0 else None
-        check(
-            LIB.spmvb_spmv_sell(
-                m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
-                ptr(wide), n_wide, ptr(first_piece), n_pieces, max_narrow, ptr(xd), ptr(y), sp, s,
-            )
-        )
+        name, args = _args_sell(m, xd, y, sp, None)
+        check(getattr(LIB, name)(*args, s))
 
     return _run(m, x, out, scale, launch)
 
 
-def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = ELL part + COO tail (kernels.py:177-199), one fused kernel."""
+def _args_hyb(m: HybMatrix, xd, y, sp, scratch):
     t = m.coo_tail
     plan = m.chunk_plan()
+    cr, cv = scratch
+    return "spmvb_spmv_hyb", (m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), t.nnz, ptr(m.tail_ptr),
+                              ptr(t.col), ptr(t.data), ptr(plan.nz_rows), plan.n_nz, ptr(plan.chunk_row), ptr(cr),
+                              ptr(cv), ptr(xd), ptr(y), sp)
+
+
+def _scratch_hyb(m: HybMatrix):
+    return m.chunk_plan().scratch(m.device)
+
+
+def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None):
+    """y = ELL part + COO tail (kernels.py:177-199), one fused kernel."""
+    m.chunk_plan()
 
     def launch(xd, y, sp, s):
-        cr, cv = plan.scratch(m.device)
-        check(
-            LIB.spmvb_spmv_hyb(
-                m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), t.nnz, ptr(m.tail_ptr), ptr(t.col),
-                ptr(t.data), ptr(plan.nz_rows), plan.n_nz, ptr(plan.chunk_row), ptr(cr), ptr(cv), ptr(xd), ptr(y),
-                sp, s,
-            )
-        )
+        name, args = _args_hyb(m, xd, y, sp, _scratch_hyb(m))
+        check(getattr(LIB, name)(*args, s))
 
     return _run(m, x, out, scale, launch)
 
@@ -302,6 +324,79 @@ _KERNELS = {
     FormatTag.SELL: (SellMatrix, spmv_sell),
     FormatTag.HYB: (HybMatrix, spmv_hyb),
 }
+
+
+_BINDERS = {
+    FormatTag.CSR: (_args_csr, _scratch_csr),
+    FormatTag.CSR5: (_args_csr5, _scratch_csr5),
+    FormatTag.ELL: (_args_ell, lambda m: None),
+    FormatTag.SELL: (_args_sell, lambda m: None),
+    FormatTag.HYB: (_args_hyb, _scratch_hyb),
+}
+
+
+class BoundCall:
+    """One library launch with every argument resolved in advance: calling it
+    is one ctypes call (no tensor checks, no allocation, no device context).
+    The buffers it was bound to must stay alive and in place; the stream is
+    the one current when it was bound."""
+
+    __slots__ = ("_fn", "_args", "_keep", "stream")
+
+    def __init__(self, name: str, args: tuple, stream: int, keep=()):
+        self._fn = getattr(_lib.load(), name)
+        self._args = tuple(args) + (stream,)
+        self._keep = keep
+        self.stream = stream
+
+    def __call__(self) -> None:
+        st = self._fn(*self._args)
+        if st:
+            check(st)
+
+
+def bind(tag: FormatTag, m: FormatMatrix, x: torch.Tensor, out: torch.Tensor, scale: torch.Tensor | None = None
+         ) -> BoundCall:
+    """A prepared ``spmv(tag, m, x, out=out, scale=scale)`` on device buffers
+    (the same kernels and results, bit for bit) for repeated calls on the same
+    buffers, e.g. every step of a power iteration: the per-call host work of
+    the generic entry point (argument checks, scratch allocation, device
+    context, stream lookup) is done once here.  ``x``/``out``: contiguous
+    float64 CUDA tensors of n_cols / n_rows elements on the matrix's device;
+    ``scale``: a device scalar or None."""
+    tag = FormatTag(tag)
+    cls, _ = _KERNELS[tag]
+    if not isinstance(m, cls):
+        raise ValueError(f"format tag {tag.value!r} does not match {type(m).__name__}")
+    for t, n, what in ((x, m.n_cols, "x"), (out, m.n_rows, "out")):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                and t.numel() == n and t.device == m.device):
+            raise ValueError(f"{what} must be a contiguous float64 CUDA tensor of {n} elements on {m.device}")
+    if scale is not None and not (scale.is_cuda and scale.dtype == torch.float64 and scale.numel() >= 1):
+        raise ValueError("scale must be a float64 CUDA scalar")
+    args_fn, scratch_fn = _BINDERS[tag]
+    scratch = scratch_fn(m)
+    name, args = args_fn(m, x, out, ptr(scale) if scale is not None else None, scratch)
+    return BoundCall(name, args, _lib.stream(m.device), keep=(m, x, out, scale, scratch))
+
+
+class SpmvOperator:
+    """``op(x, out, scale)`` = ``spmv(tag, m, x, out=out, scale=scale)``, a
+    ``local_spmv`` for ``dist.PowerIteration`` whose ``bind`` lets the
+    iteration prepare its launches once per buffer pair (``kernels.bind``)."""
+
+    def __init__(self, tag: FormatTag, m: FormatMatrix):
+        self.tag = FormatTag(tag)
+        cls, _ = _KERNELS[self.tag]
+        if not isinstance(m, cls):
+            raise ValueError(f"format tag {self.tag.value!r} does not match {type(m).__name__}")
+        self.m = m
+
+    def __call__(self, x, out, scale=None):
+        return spmv(self.tag, self.m, x, out=out, scale=scale)
+
+    def bind(self, x, out, scale=None) -> BoundCall:
+        return bind(self.tag, self.m, x, out, scale)
 
 
 def spmv(tag: FormatTag, m: FormatMatrix, x, workers: int = 1, **kw):

@@ -27,7 +27,7 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .coo import canonicalize
 from .formats import CsrMatrix, FormatTag, convert, to_csr
-from .kernels import spmv
+from .kernels import SpmvOperator, bind, spmv
 
 __all__ = ["DegreeOrder", "RelabelledMatrix", "power_iteration"]
 
@@ -116,6 +116,12 @@ class RelabelledMatrix:
         """``y' = scale * (P A P^T) x'`` on device vectors in the new ids."""
         return spmv(self.tag, self.inner, xp, out=out, scale=scale)
 
+    def bind(self, xp: torch.Tensor, out: torch.Tensor, scale=None):
+        """A prepared ``spmv(xp, out, scale)`` (kernels.bind) in the new ids."""
+        return bind(self.tag, self.inner, xp, out, scale)
+
+    __call__ = spmv
+
     def spmv_original(self, x: torch.Tensor) -> torch.Tensor:
         """``A x`` in the original ids (two permutation gathers around the SpMV)."""
         return self.order.to_old(self.spmv(self.order.to_new(x)))
@@ -135,11 +141,10 @@ def power_iteration(a, x0, steps: int, tag="csr5", *, relabel: bool = True, grap
     x0 = torch.as_tensor(x0, dtype=torch.float64).to(dev).reshape(-1)
     if relabel:
         rm = RelabelledMatrix(tag, csr, **convert_kw)
-        pi = PowerIteration(lambda xv, out, scale: rm.spmv(xv, out, scale), [0, csr.n_rows], 0, 1, dev,
-                            rm.order.to_new(x0))
+        pi = PowerIteration(rm, [0, csr.n_rows], 0, 1, dev, rm.order.to_new(x0))
         pi.run(steps, graph=graph)
         return rm.order.to_old(pi.normalized()), pi.eigenvalue_estimate()
     m = convert(tag, csr, **convert_kw)
-    pi = PowerIteration(lambda xv, out, scale: spmv(tag, m, xv, out=out, scale=scale), [0, csr.n_rows], 0, 1, dev, x0)
+    pi = PowerIteration(SpmvOperator(tag, m), [0, csr.n_rows], 0, 1, dev, x0)
     pi.run(steps, graph=graph)
     return pi.normalized(), pi.eigenvalue_estimate()

@@ -20,30 +20,35 @@ WANT = {
 
 
 def raw(path):
+    """One dict per profiled kernel of the report."""
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = {}
-    for h, u, v in zip(hdr, units, vals):
-        if h in WANT:
-            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
-                     "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "hz": 1.0, "Mhz": 1e6,
-                     "Ghz": 1e9}.get(u, 1.0)
-            try:
-                d[WANT[h]] = float(v.replace(",", "")) * scale
-            except ValueError:
-                pass
-        if h == "Kernel Name":
-            d["kernel"] = v
-    return d
+    hdr, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        d = {}
+        for h, u, v in zip(hdr, units, vals):
+            if h in WANT:
+                scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                         "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1.0, "KB": 1e3, "MB": 1e6,
+                         "GB": 1e9, "hz": 1.0, "Mhz": 1e6, "Ghz": 1e9, "Hz": 1.0, "MHz": 1e6, "GHz": 1e9}.get(u, 1.0)
+                try:
+                    d[WANT[h]] = float(v.replace(",", "")) * scale
+                except ValueError:
+                    pass
+            if h == "Kernel Name":
+                d["kernel"] = v
+        res.append(d)
+    return res
 
 
-print("| report | kernel | time (us) | DRAM read+write (MB) | DRAM % peak | L1TEX % | L2 % | L1 hit % | L2 hit % | warps active % | SM clock (MHz) |")
-print("|---|---|---|---|---|---|---|---|---|---|---|")
+print("| report | # | kernel | time (us) | DRAM read+write (MB) | DRAM % peak | L1TEX % | L2 % | L1 hit % | L2 hit % | warps active % | SM clock (MHz) |")
+print("|---|---|---|---|---|---|---|---|---|---|---|---|")
 for p in sys.argv[1:]:
-    d = raw(p)
     name = p.rsplit("/", 1)[-1].replace(".ncu-rep", "")
-    tot = (d.get("dram_rd", 0) + d.get("dram_wr", 0)) / 1e6
-    print(f"| {name} | `{d.get('kernel', '?')[:40]}` | {d.get('dur_us', 0):.1f} | {tot:.1f} | {d.get('dram_pct', 0):.1f} | "
-          f"{d.get('l1tex_pct', 0):.1f} | {d.get('l2_pct', 0):.1f} | {d.get('l1_hit', 0):.1f} | {d.get('l2_hit', 0):.1f} | "
-          f"{d.get('occ_pct', 0):.1f} | {d.get('sm_hz', 0) / 1e6:.0f} |")
+    for i, d in enumerate(raw(p)):
+        tot = (d.get("dram_rd", 0) + d.get("dram_wr", 0)) / 1e6
+        print(f"| {name} | {i} | `{d.get('kernel', '?')[:44]}` | {d.get('dur_us', 0):.1f} | {tot:.1f} | "
+              f"{d.get('dram_pct', 0):.1f} | {d.get('l1tex_pct', 0):.1f} | {d.get('l2_pct', 0):.1f} | "
+              f"{d.get('l1_hit', 0):.1f} | {d.get('l2_hit', 0):.1f} | {d.get('occ_pct', 0):.1f} | "
+              f"{d.get('sm_hz', 0) / 1e6:.0f} |")

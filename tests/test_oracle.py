@@ -190,3 +190,31 @@ def test_model_loading_and_prediction_match_reference(golden):
         assert predict(model, fv).value == str(g["predicted"]), name
         checked += 1
     assert checked >= 20
+
+
+def test_full_rmat_csr_builder_matches_port():
+    """oracle/rmat_sample.c:rmat_csr (the CPU reference arm's whole-matrix
+    build) equals the port's canonicalize/to_csr of the host-regenerated
+    draws, bit for bit."""
+    from oracle import cpu_baseline, synth_ref
+
+    for scale, ef, seed in [(11, 8, 3), (13, 16, 105), (9, 1, 7)]:
+        p, i, d = cpu_baseline.rmat_full_csr(scale, ef, seed, threads=4)
+        hr, hc, hv = synth_ref.rmat(scale, ef, seed)
+        n = 1 << scale
+        r, c, v = port.canonicalize(hr, hc, hv, n, n)
+        p2, i2, d2 = port.to_csr(r, c, v, n)
+        assert np.array_equal(p, p2) and np.array_equal(i, i2) and d.tobytes() == d2.tobytes()
+
+
+def test_row_subset_matches_port():
+    from oracle import cpu_baseline, synth_ref
+
+    rows, ptr, ind, dat = cpu_baseline.rmat_row_subset(12, 8, 3, keep_mod=5, ranges=[(0, 3), (2000, 2100)], threads=3)
+    hr, hc, hv = synth_ref.rmat(12, 8, 3)
+    r, c, v = port.canonicalize(hr, hc, hv, 1 << 12, 1 << 12)
+    P, I, D = port.to_csr(r, c, v, 1 << 12)
+    assert {0, 1, 2, 2050} <= set(rows.tolist())
+    for k, row in enumerate(rows):
+        assert np.array_equal(I[P[row]:P[row + 1]], ind[ptr[k]:ptr[k + 1]])
+        assert D[P[row]:P[row + 1]].tobytes() == dat[ptr[k]:ptr[k + 1]].tobytes()
