@@ -860,7 +860,9 @@ def main():
                     help="N > 1: also time the peer-memory exchange (symmetric memory) next to the default")
     ap.add_argument("--exchange", choices=["allgatherv", "sparse", "p2p"], default="allgatherv",
                     help="x exchange between row blocks (N > 1): the north-star all-gather of x (default), or "
-                         "only the entries each shard reads; the other one is timed too and reported")
+                         "only the entries each shard reads; the other one is timed too and reported.  p2p "
+                         "(our kernels over peer memory) is EXPERIMENTAL: only one GPU has been available to this "
+                         "project, so it is verified at world 1 and by tests/test_gpu_multi.py where 2 GPUs exist")
     ap.add_argument("--p2p-unfused", action="store_true",
                     help="p2p exchange with a separate push kernel per row range instead of the fused SpMV+push")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)
