@@ -1,7 +1,7 @@
 // Synthetic inputs for the benchmark configurations:
 // R-MAT edge lists and uniform vectors from a counter-based hash, so the
 // same matrix can be regenerated bit-identically on the host
-// (oracle/synth.py, oracle/rmat_sample.c) for parity checks and the CPU
+// (oracle/synth_ref.py, oracle/rmat_sample.c) for parity checks and the CPU
 // baseline sample.
 //
 // hash(seed, e, l) = mix64(mix64(seed) ^ (e * 64 + l)), mix64 = splitmix64
