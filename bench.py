@@ -409,10 +409,23 @@ def run_ours(args):
     from paper_1805_11938_b200.relabel import DegreeOrder
 
     world, rank, local = dist_env()
+    local = local % max(torch.cuda.device_count(), 1) if args.dist_backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+
+    def coll(fn, t, *a, **k):
+        """A collective on a CUDA tensor (staged through the host under gloo)."""
+        if args.dist_backend == "gloo":
+            h = t.cpu()
+            fn(h, *a, **k)
+            t.copy_(h)
+        else:
+            fn(t, *a, **k)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # gloo: a code-path check of N > 1 on fewer GPUs (host-staged exchange; timings meaningless)
+            dist.init_process_group("gloo")
     elif args.exchange == "p2p":
         # the peer-memory exchange rendezvouses its symmetric buffers over a
         # process group: a one-rank group on 127.0.0.1 for a single GPU
@@ -508,7 +521,7 @@ def run_ours(args):
     if world > 1:
         names = [variant_label(t_, k_) for t_, k_ in CANDIDATES]
         choice = torch.tensor([names.index(variant_label(tag, kw))], device=dev)
-        dist.broadcast(choice, 0)
+        coll(dist.broadcast, choice, 0)
         want_tag, want_kw = CANDIDATES[int(choice.item())]
         if variant_label(want_tag, want_kw) != variant_label(tag, kw):
             tag, kw = want_tag, want_kw
@@ -542,6 +555,7 @@ def run_ours(args):
     if world > 1:
         del csr_full
     torch.cuda.empty_cache()
+    y_tmp = torch.empty(m.n_rows, dtype=torch.float64, device=dev)  # the run shard's rows (relabelled bounds)
     t_kernel = event_time(lambda: sp.spmv(tag, m, x_run, out=y_tmp), reps=args.kernel_reps)
 
     # a shard whose format bytes are under 4x L2 would be partly served from
@@ -620,7 +634,7 @@ def run_ours(args):
     # collectives, so ranks must run exactly the same number)
     n_ramp = torch.tensor([int(args.clock_ramp_s / max(t_kernel, 1e-6))], dtype=torch.int64, device=dev)
     if world > 1:
-        dist.all_reduce(n_ramp, op=dist.ReduceOp.MAX)
+        coll(dist.all_reduce, n_ramp, op=dist.ReduceOp.MAX)
     for i in range(int(n_ramp.item())):
         pi.step()
         if i % 50 == 49:
@@ -656,7 +670,7 @@ def run_ours(args):
     clk = clocks.stop()
     if world > 1:
         tt = torch.tensor([t_loop], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        coll(dist.all_reduce, tt, op=dist.ReduceOp.MAX)
         t_loop = float(tt.item())
     value = 2.0 * nnz * args.steps / t_loop / 1e9
     eig = pi.eigenvalue_estimate()
@@ -684,7 +698,7 @@ def run_ours(args):
                 ev1.record()
                 torch.cuda.synchronize()
                 tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                coll(dist.all_reduce, tt, op=dist.ReduceOp.MAX)
                 exchange[f"ms_per_step_{other}"] = float(tt.item()) / args.steps * 1e3
                 vol = vol or getattr(pj, "exchange_volume", None)
                 del pj
@@ -728,7 +742,7 @@ def run_ours(args):
     t_many = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([t_chain, t_many], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        coll(dist.all_reduce, tt, op=dist.ReduceOp.MAX)
         t_chain, t_many = float(tt[0].item()), float(tt[1].item())
     e2e = {"value": 2.0 * nnz * e2e_steps / t_chain / 1e9, "unit": "GFLOP/s",
            "h2d_bytes_per_step": int(bufs[0].numel() * 8), "d2h_bytes_per_step": int(bufs[1].numel() * 8),
@@ -820,7 +834,7 @@ def launch_ranks(args):
     if args.gpus == 1:
         return
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and args.dist_backend == "nccl":
         sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}\n")
         sys.exit(2)
     import socket
@@ -865,6 +879,8 @@ def main():
                          "project, so it is verified at world 1 and by tests/test_gpu_multi.py where 2 GPUs exist")
     ap.add_argument("--p2p-unfused", action="store_true",
                     help="p2p exchange with a separate push kernel per row range instead of the fused SpMV+push")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: ranks may share GPUs (checks the N > 1 code path on a small box; not a measurement)")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)
     ap.add_argument("--cpu-sample", choices=["auto", "full", "rows"], default="auto",
                     help="CPU reference on R-MAT: the whole matrix (auto: when the host RAM allows) or a row sample")

@@ -52,13 +52,16 @@ class Guards:
         return view
 
     def check(self):
-        for base, n, head in self.live:
+        live, self.live = self.live, []
+        bad = []
+        for base, n, head in live:
             lo, hi = base[:GUARD], base[GUARD + n:]
             same = lambda a, b: torch.equal(a.view(torch.uint8) if a.dtype != torch.bool else a,  # noqa: E731
                                             b.view(torch.uint8) if b.dtype != torch.bool else b)
-            assert same(lo, head) and same(hi, head), f"guard band overwritten next to a {base.dtype} buffer of {n}"
+            if not (same(lo, head) and same(hi, head)):
+                bad.append(f"{base.dtype}[{n}]")
             self.checked += 1
-        self.live.clear()
+        assert not bad, f"guard band overwritten next to {len(bad)} buffer(s): {', '.join(bad[:8])}"
 
 
 @pytest.fixture
