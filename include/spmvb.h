@@ -276,21 +276,27 @@ int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* 
                    const double* scale, void* stream);
 
 /* spmv_sell (kernels.py:119-136); perm may be NULL for sigma == 0.  Slices
- * up to SPMVB_SELL_WIDE_COLS wide (or taller than 128 rows) are summed one
- * thread per row, sequentially and without FMA: bit-identical to the
- * reference.  Wider slices (power-law rows) are listed by
- * spmvb_sell_wide_plan and summed by a CTA each (within tolerance). */
+ * up to wide_cols (>= SPMVB_SELL_WIDE_COLS; 0 = that default) wide, or taller
+ * than 128 rows, are summed one thread per row, sequentially and without
+ * FMA: bit-identical to the reference.  Wider slices (power-law rows) are
+ * listed by spmvb_sell_wide_plan (same wide_cols) and summed by a CTA each
+ * (within tolerance).  A larger wide_cols pays on big matrices, where the
+ * long per-thread rows hide behind the rest of the grid (the library picks
+ * it from nnz: formats.SellMatrix.wide_plan). */
+#ifndef SPMVB_SELL_WIDE_COLS
 #define SPMVB_SELL_WIDE_COLS 256
+#endif
 /* Also reports (host, may be NULL) the widest slice left to the per-row
  * kernel, which spmvb_spmv_sell uses to pick its slot loop (-1 = unknown),
  * and (first_piece_out: device, n_slices entries; n_pieces: host) how the
  * wide slices split into pieces of ~32K cells, one CTA each. */
-int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out, int64_t* n_wide,
-                         int64_t* max_narrow_width, int32_t* first_piece_out, int64_t* n_pieces, void* stream);
+int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int64_t wide_cols, int32_t* wide_out,
+                         int64_t* n_wide, int64_t* max_narrow_width, int32_t* first_piece_out, int64_t* n_pieces,
+                         void* stream);
 int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                     const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
-                    const int32_t* first_piece, int64_t n_pieces, int64_t max_narrow_width, const double* x,
-                    double* y, const double* scale, void* stream);
+                    const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols, int64_t max_narrow_width,
+                    const double* x, double* y, const double* scale, void* stream);
 
 /* ||y||^2 over n entries into *out (device), deterministic two-level sum.
  * Used by power iteration. */
@@ -322,13 +328,15 @@ int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t n, double* 
  * on R-MAT: CSR5 SpMV ~13 % faster at scale 25); the reference's arrays are
  * left untouched and the iterate is mapped with spmvb_gather_f64.
  * spmvb_degree_order: new ids sorted by (row empty, -(row degree + column
- * degree)), stable by old id, so every empty row is last.  perm[new] = old,
+ * degree)) (mode 0) or by (row empty, -row degree, -column degree) (mode 1:
+ * rows in exact descending length), stable by old id, so every empty row is
+ * last.  perm[new] = old,
  * new_id[old] = new (n entries each); *n_nonempty (host) = non-empty rows.
  * Synchronizes.
  * spmvb_relabel_csr: the entries of P A P^T as triplets in the old CSR
  * order (row_out[k] = new_id[row(k)], col_out[k] = new_id[col[k]],
  * val_out[k] = val[k]); canonicalize them to get its CSR. */
-int spmvb_degree_order(int64_t n, const int32_t* ptr, const int32_t* col, int64_t nnz, int32_t* perm,
+int spmvb_degree_order(int64_t n, const int32_t* ptr, const int32_t* col, int64_t nnz, int mode, int32_t* perm,
                        int32_t* new_id, int64_t* n_nonempty, void* stream);
 int spmvb_relabel_csr(int64_t n, const int32_t* ptr, const int32_t* col, const double* val, int64_t nnz,
                       const int32_t* new_id, int32_t* row_out, int32_t* col_out, double* val_out, void* stream);

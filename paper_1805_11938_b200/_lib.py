@@ -100,8 +100,9 @@ SIGNATURES: dict[str, tuple] = {
          vp, vp, vp],
     ),
     "spmvb_spmv_ell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp]),
-    "spmvb_sell_wide_plan": (c_int, [c_i64, c_i64, vp, vp, P_i64, P_i64, vp, P_i64, vp]),
-    "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, c_i64, vp, vp, vp, vp]),
+    "spmvb_sell_wide_plan": (c_int, [c_i64, c_i64, vp, c_i64, vp, P_i64, P_i64, vp, P_i64, vp]),
+    "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, c_i64, c_i64, vp, vp, vp,
+                                vp]),
     "spmvb_sumsq": (c_int, [vp, c_i64, vp, vp]),
     "spmvb_inv_sqrt": (c_int, [vp, vp, vp]),
     "spmvb_norm_ws_bytes": (c_i64, []),
@@ -109,7 +110,7 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_column_set": (c_int, [vp, c_i64, c_i64, vp, P_i64, vp]),
     "spmvb_gather_f64": (c_int, [vp, c_i64, vp, c_i64, vp, vp]),
     "spmvb_scatter_f64": (c_int, [vp, vp, c_i64, vp, vp]),
-    "spmvb_degree_order": (c_int, [c_i64, vp, vp, c_i64, vp, vp, P_i64, vp]),
+    "spmvb_degree_order": (c_int, [c_i64, vp, vp, c_i64, c_int, vp, vp, P_i64, vp]),
     "spmvb_relabel_csr": (c_int, [c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp]),
     "spmvb_push_rows": (c_int, [vp, c_i64, vp, c_int, c_i64, vp]),
     "spmvb_sum_inv_sqrt": (c_int, [vp, c_int, vp, vp, vp]),

@@ -586,8 +586,9 @@ extern "C" int spmvb_sell_fill(int64_t n_rows, const int32_t* ptr, const int32_t
     const int64_t n_slices = (n_rows + c - 1) / c;
     DevBuf<int32_t> wide(n_slices, s), first_piece(n_slices, s);
     int64_t n_wide = 0, n_pieces = 0;
-    if (const int st = spmvb_sell_wide_plan(n_rows, c, widths, wide.get(), &n_wide, nullptr, first_piece.get(),
-                                            &n_pieces, s)) {
+    // the fill's own split (default width): independent of the SpMV's wide_cols
+    if (const int st = spmvb_sell_wide_plan(n_rows, c, widths, SPMVB_SELL_WIDE_COLS, wide.get(), &n_wide, nullptr,
+                                            first_piece.get(), &n_pieces, s)) {
       const std::string msg = spmvb_last_error();
       fail(st, "%s", msg.c_str());
     }

@@ -22,14 +22,18 @@ __global__ void k_col_degree(const int32_t* __restrict__ col, int64_t nnz, int32
     atomicAdd(deg + ld_stream(col + k), 1);
 }
 
-// key(i) = empty(i) << dbits | (max_sum - (rowdeg(i) + coldeg(i)))
+// mode 0: key(i) = empty(i) << dbits | (max_sum - (rowdeg(i) + coldeg(i)))
+// mode 1: key(i) = empty(i) << dbits | (max_rd - rowdeg(i)) << cbits | (max_cd - coldeg(i))
+//         (rows in exact descending length: SELL slices need no sigma window)
 __global__ void k_degree_keys(const int32_t* __restrict__ ptr, const int32_t* __restrict__ coldeg, int64_t n,
-                              uint64_t max_sum, int dbits, uint64_t* __restrict__ keys) {
+                              int mode, uint64_t max_a, uint64_t max_b, int cbits, int dbits,
+                              uint64_t* __restrict__ keys) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
     const uint64_t rd = static_cast<uint64_t>(ptr[i + 1] - ptr[i]);
-    const uint64_t sum = rd + static_cast<uint64_t>(coldeg[i]);
-    keys[i] = (static_cast<uint64_t>(rd == 0) << dbits) | (max_sum - sum);
+    const uint64_t cd = static_cast<uint64_t>(coldeg[i]);
+    const uint64_t low = mode == 0 ? max_a - (rd + cd) : ((max_a - rd) << cbits) | (max_b - cd);
+    keys[i] = (static_cast<uint64_t>(rd == 0) << dbits) | low;
   }
 }
 
@@ -56,11 +60,12 @@ __global__ void k_relabel_entries(int64_t nnz, const int32_t* __restrict__ new_i
 
 }  // namespace
 
-extern "C" int spmvb_degree_order(int64_t n, const int32_t* ptr, const int32_t* col, int64_t nnz, int32_t* perm,
-                                  int32_t* new_id, int64_t* n_nonempty, void* stream) {
+extern "C" int spmvb_degree_order(int64_t n, const int32_t* ptr, const int32_t* col, int64_t nnz, int mode,
+                                  int32_t* perm, int32_t* new_id, int64_t* n_nonempty, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n < 0 || nnz < 0) fail(SPMVB_INVALID_ARG, "negative size");
+    if (mode != 0 && mode != 1) fail(SPMVB_INVALID_ARG, "mode must be 0 (row + column degree) or 1 (row degree)");
     if (!n_nonempty) fail(SPMVB_INVALID_ARG, "n_nonempty is required");
     *n_nonempty = 0;
     if (n == 0) return;
@@ -71,21 +76,28 @@ extern "C" int spmvb_degree_order(int64_t n, const int32_t* ptr, const int32_t* 
       SPMVB_LAUNCHED("k_col_degree");
     }
     const int32_t* dg = deg.get();
-    DevBuf<int64_t> stats(2, s);
+    DevBuf<int64_t> stats(4, s);
     device_reduce<int64_t>(
         n, [=] __device__(int64_t i) { return static_cast<int64_t>(ptr[i + 1] - ptr[i]) + dg[i]; }, OpMax{},
         (int64_t)0, stats.get(), s);
     device_reduce<int64_t>(
         n, [=] __device__(int64_t i) { return static_cast<int64_t>(ptr[i + 1] > ptr[i]); }, OpSum{}, (int64_t)0,
         stats.get() + 1, s);
-    int64_t h[2];
-    copy_to_host(h, stats.get(), 2, s);
+    device_reduce<int64_t>(
+        n, [=] __device__(int64_t i) { return static_cast<int64_t>(ptr[i + 1] - ptr[i]); }, OpMax{}, (int64_t)0,
+        stats.get() + 2, s);
+    device_reduce<int64_t>(
+        n, [=] __device__(int64_t i) { return static_cast<int64_t>(dg[i]); }, OpMax{}, (int64_t)0, stats.get() + 3, s);
+    int64_t h[4];
+    copy_to_host(h, stats.get(), 4, s);
     *n_nonempty = h[1];
-    const uint64_t max_sum = static_cast<uint64_t>(h[0]);
-    const int dbits = bits_for(max_sum);
+    const uint64_t max_a = static_cast<uint64_t>(mode == 0 ? h[0] : h[2]);
+    const uint64_t max_b = static_cast<uint64_t>(h[3]);
+    const int cbits = bits_for(max_b);
+    const int dbits = mode == 0 ? bits_for(max_a) : bits_for(max_a) + cbits;
     DevBuf<uint64_t> ka(n, s), kb(n, s);
     DevBuf<uint32_t> vb(n, s), vs(n, s);
-    k_degree_keys<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(ptr, dg, n, max_sum, dbits, ka.get());
+    k_degree_keys<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(ptr, dg, n, mode, max_a, max_b, cbits, dbits, ka.get());
     SPMVB_LAUNCHED("k_degree_keys");
     RadixSortResult rs = radix_sort_pairs(ka.get(), nullptr, kb.get(), vb.get(), vs.get(), n, dbits + 1, s);
     k_invert_perm<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(rs.vals, n, perm, new_id);

@@ -133,53 +133,54 @@ __device__ __forceinline__ void fold_chains(int64_t begin, int64_t end, Key key_
 // x gathers are consumed (unpredicated full steps, then a scalar tail).
 // Two alternating buffers: C3 ELL back-to-back 37.5 -> 35.1 us, L2-flushed
 // 43.3 -> 43.1 us, against one buffer copied forward each step.
-template <bool CACHED = false>
+template <bool CACHED = false, int D = 4>
 __device__ __forceinline__ double seq_slots(int64_t k, int64_t stride, int64_t base, const int32_t* __restrict__ idx,
                                             const double* __restrict__ val, const double* __restrict__ x) {
-  // CACHED: slot loads through L1 (narrow SELL slices, see seq_slots4)
+  // CACHED: slot loads through L1 (narrow SELL slices, see seq_slots4).
+  // D: slots per step (the prefetch depth; D gathers in flight per thread)
   auto li = [](const int32_t* p) { return CACHED ? __ldg(p) : ld_stream(p); };
   auto lv = [](const double* p) { return CACHED ? __ldg(p) : ld_stream(p); };
-  // two 4-slot buffers used alternately (a 2x-unrolled loop) so that no
+  // two D-slot buffers used alternately (a 2x-unrolled loop) so that no
   // register is copied while its prefetched load is still pending: a
   // copy would wait for the load and end the overlap
-  auto load = [&](int64_t j, int32_t (&c)[4], double (&v)[4]) {
+  auto load = [&](int64_t j, int32_t (&c)[D], double (&v)[D]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < D; ++u) {
       c[u] = li(idx + base + (j + u) * stride);
       v[u] = lv(val + base + (j + u) * stride);
     }
   };
   double acc = 0.0;
-  auto consume = [&](const int32_t (&c)[4], const double (&v)[4]) {
-    double xv[4];
+  auto consume = [&](const int32_t (&c)[D], const double (&v)[D]) {
+    double xv[D];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = ldx(x, c[u]);
+    for (int u = 0; u < D; ++u) xv[u] = ldx(x, c[u]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    for (int u = 0; u < D; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
   };
   int64_t j = 0;
-  if (k >= 4) {
-    int32_t ca[4], cb[4];
-    double va[4], vb[4];
+  if (k >= D) {
+    int32_t ca[D], cb[D];
+    double va[D], vb[D];
     load(0, ca, va);
-    for (;;) {  // ca/va hold slots j..j+3
-      if (j + 8 <= k) {
-        load(j + 4, cb, vb);
+    for (;;) {  // ca/va hold slots j..j+D-1
+      if (j + 2 * D <= k) {
+        load(j + D, cb, vb);
         consume(ca, va);
-        j += 4;
+        j += D;
       } else {
         consume(ca, va);
-        j += 4;
+        j += D;
         break;
       }
-      // cb/vb hold slots j..j+3
-      if (j + 8 <= k) {
-        load(j + 4, ca, va);
+      // cb/vb hold slots j..j+D-1
+      if (j + 2 * D <= k) {
+        load(j + D, ca, va);
         consume(cb, vb);
-        j += 4;
+        j += D;
       } else {
         consume(cb, vb);
-        j += 4;
+        j += D;
         break;
       }
     }

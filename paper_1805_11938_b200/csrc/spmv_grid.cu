@@ -25,14 +25,21 @@ __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict_
 }
 
 // =============================================================== SELL ====
+#ifndef SPMVB_SELL_PF
+#define SPMVB_SELL_PF 4  // slots per prefetch step of the narrow SELL loop (MODE 2/3)
+#endif
+#ifndef SPMVB_SELL_WIDE_U
+#define SPMVB_SELL_WIDE_U 8  // column cells in flight per thread in k_sell_wide_part
+#endif
 // MODE 0: four slots per step; 1: the same through L1 (c < 8); 2: with the
 // next four slots prefetched (rows of 8 slots or more); 3: prefetched and
 // through L1 (c < 8, rows of 8 slots or more).
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? 5 : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
+__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? (SPMVB_SELL_PF > 4 ? 4 : 5) : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
-                            const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
+                            const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p,
+                            int64_t wide_cols) {
   pdl_wait();
   const double s = load_scale(scale_p);
   const int32_t c32 = static_cast<int32_t>(c);  // n_rows < 2^31: 32-bit slice arithmetic
@@ -42,9 +49,9 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? 5 : 4)) k_sp
     const int32_t sl = p32 / c32, local = p32 - sl * c32;
     const int64_t rows_s = (static_cast<int64_t>(sl) + 1) * c <= n_rows ? c : n_rows - static_cast<int64_t>(sl) * c;
     const int64_t w = widths[sl];
-    if (w > SPMVB_SELL_WIDE_COLS && rows_s <= 128) continue;  // k_spmv_sell_wide's slice
+    if (w > wide_cols && rows_s <= 128) continue;  // k_sell_wide_part's slice
     const int64_t base = slice_off[sl] + local;
-    const double acc = MODE >= 2 ? seq_slots<MODE == 3>(w, rows_s, base, idx, val, x)
+    const double acc = MODE >= 2 ? seq_slots<MODE == 3, SPMVB_SELL_PF>(w, rows_s, base, idx, val, x)
                                  : seq_slots4<MODE == 1>(w, rows_s, base, idx, val, x);
     const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
     y[r] = scale_p ? s * acc : acc;
@@ -105,16 +112,18 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
     if (sub < nsub) {
       const int64_t st = static_cast<int64_t>(nsub) * rows_s;
       int64_t j = j0 + sub;
-      for (; j + 3 * nsub < j1; j += 4 * nsub) {
+      constexpr int WU = SPMVB_SELL_WIDE_U;
+      for (; j + (WU - 1) * nsub < j1; j += WU * nsub) {
         const int64_t o = base + j * rows_s + l;
-        const double v0 = ld_stream(val + o), v1 = ld_stream(val + o + st);
-        const double v2 = ld_stream(val + o + 2 * st), v3 = ld_stream(val + o + 3 * st);
-        const int32_t c0 = ld_stream(idx + o), c1 = ld_stream(idx + o + st);
-        const int32_t c2 = ld_stream(idx + o + 2 * st), c3 = ld_stream(idx + o + 3 * st);
-        acc += v0 * ldx(x, c0);
-        acc += v1 * ldx(x, c1);
-        acc += v2 * ldx(x, c2);
-        acc += v3 * ldx(x, c3);
+        double v[WU];
+        int32_t cc[WU];
+#pragma unroll
+        for (int u = 0; u < WU; ++u) {
+          v[u] = ld_stream(val + o + u * st);
+          cc[u] = ld_stream(idx + o + u * st);
+        }
+#pragma unroll
+        for (int u = 0; u < WU; ++u) acc += v[u] * ldx(x, cc[u]);
       }
       for (; j < j1; j += nsub) {
         const int64_t o = base + j * rows_s + l;
@@ -155,28 +164,31 @@ __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __re
 }
 
 __global__ void k_sell_mark_wide(const int64_t* __restrict__ widths, int64_t n_rows, int64_t c, int64_t n_slices,
-                                 uint8_t* __restrict__ flag) {
+                                 int64_t wide_cols, uint8_t* __restrict__ flag) {
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n_slices;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t rows_s = (s + 1) * c <= n_rows ? c : n_rows - s * c;
-    flag[s] = (widths[s] > SPMVB_SELL_WIDE_COLS && rows_s <= 128) ? 1 : 0;
+    flag[s] = (widths[s] > wide_cols && rows_s <= 128) ? 1 : 0;
   }
 }
 
 }  // namespace
 
-extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int32_t* wide_out,
-                                    int64_t* n_wide, int64_t* max_narrow_width, int32_t* first_piece_out,
-                                    int64_t* n_pieces, void* stream) {
+extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int64_t wide_cols,
+                                    int32_t* wide_out, int64_t* n_wide, int64_t* max_narrow_width,
+                                    int32_t* first_piece_out, int64_t* n_pieces, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
+    if (wide_cols <= 0) wide_cols = SPMVB_SELL_WIDE_COLS;
+    if (wide_cols < SPMVB_SELL_WIDE_COLS) fail(SPMVB_INVALID_ARG, "wide_cols must be >= %d", SPMVB_SELL_WIDE_COLS);
     *n_wide = 0;
     if (max_narrow_width) *max_narrow_width = 0;
     if (n_pieces) *n_pieces = 0;
     if (n_rows <= 0 || c < 1) return;
     const int64_t n_slices = (n_rows + c - 1) / c;
     DevBuf<uint8_t> flag(n_slices, s);
-    k_sell_mark_wide<<<grid_for(n_slices, 256, 148 * 16), 256, 0, s>>>(widths, n_rows, c, n_slices, flag.get());
+    k_sell_mark_wide<<<grid_for(n_slices, 256, 148 * 16), 256, 0, s>>>(widths, n_rows, c, n_slices, wide_cols,
+                                                                      flag.get());
     SPMVB_LAUNCHED("k_sell_mark_wide");
     const uint8_t* f = flag.get();
     DevBuf<int32_t> total(1, s);
@@ -226,12 +238,13 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
 
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
-                               int64_t n_wide, const int32_t* first_piece, int64_t n_pieces,
+                               int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
                                int64_t max_narrow_width, const double* x, double* y, const double* scale,
                                void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
+    if (wide_cols <= 0) wide_cols = SPMVB_SELL_WIDE_COLS;
     // c < 8: slot loads through L1 (the other half of each index sector is
     // the next slot's); rows of 8 or more slots: next four slots prefetched
     const unsigned g = grid_for(n_rows, 256);
@@ -239,7 +252,7 @@ extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths,
     // 36.9 / 50.2 us L2-flushed against mode 1)
     const bool wide_rows = max_narrow_width >= 8 || max_narrow_width < 0;
     auto kern = c < 8 ? (wide_rows ? k_spmv_sell<3> : k_spmv_sell<1>) : (wide_rows ? k_spmv_sell<2> : k_spmv_sell<0>);
-    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale);
+    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale, wide_cols);
     SPMVB_LAUNCHED("k_spmv_sell");
     if (n_wide > 0) {
       if (!first_piece || n_pieces < n_wide) fail(SPMVB_INVALID_ARG, "wide-slice piece plan missing");

@@ -275,20 +275,37 @@ class SellMatrix:
         self._host = None
         self._wide = None
 
+    def wide_cols(self) -> int:
+        """Slices up to this width are summed one thread per row (sequential,
+        bit-identical); wider ones by a CTA per ~32K-cell piece.  256 (the
+        header's SPMVB_SELL_WIDE_COLS) unless the matrix is big enough for
+        longer per-thread rows to hide behind the rest of the grid: about
+        twice the cells per resident thread, rounded up to a power of two,
+        at most 4096 (degree-ordered C5: 2.20 -> 2.09 ms at 4096; C4 stays
+        at 256, where 1024 would serialise it: 135 -> 222 us;
+        profiles/r02_sell_ab2.txt)."""
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        per_thread = self.total_cells / max(sms * 2048, 1)
+        w = 256
+        while w < 4096 and w < 2 * per_thread:
+            w *= 2
+        return w
+
     def wide_plan(self):
         """(wide slice list, count, widest remaining slice, first piece per
-        wide slice, piece count): slices wider than SPMVB_SELL_WIDE_COLS are
-        cut into ~32K-cell pieces, a CTA each (kernel-side, built once)."""
+        wide slice, piece count, wide_cols): slices wider than wide_cols()
+        are cut into ~32K-cell pieces, a CTA each (kernel-side, built once)."""
         if self._wide is None:
             n_slices = self.n_slices
+            wide_cols = self.wide_cols()
             lst = _i32(max(n_slices, 1), self.device)
             first = _i32(max(n_slices, 1), self.device)
             cnt, mx, npieces = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
             with torch.cuda.device(self.device):
-                check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), ptr(lst), ctypes.byref(cnt),
-                                               ctypes.byref(mx), ptr(first), ctypes.byref(npieces),
-                                               _lib.stream(self.device)))
-            self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value))
+                check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), wide_cols, ptr(lst),
+                                               ctypes.byref(cnt), ctypes.byref(mx), ptr(first),
+                                               ctypes.byref(npieces), _lib.stream(self.device)))
+            self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value), wide_cols)
         return self._wide
 
     def _host_layout(self):

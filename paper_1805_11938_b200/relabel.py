@@ -7,8 +7,9 @@ a second, relabelled copy ``P A P^T`` and runs the iteration on
 ``x' = P x``, so ``P^T x'_k`` is the same iterate as the plain iteration's
 ``x_k`` (within the SpMV tolerance: only the order of the row sums differs).
 
-The relabelling (csrc/relabel.cu) sorts ids by (row is empty, -(row degree +
-column degree)), stable by id.  On R-MAT it packs the hot columns of x into
+The relabelling (csrc/relabel.cu) sorts ids by (row is empty, -row degree,
+-column degree) (or by row + column degree), stable by id.  On R-MAT it packs
+the hot columns of x into
 the first cache lines (more L1/L2 hits per gathered 128-byte line; the C5
 SpMV is bound by the rate of distinct lines its random x gathers touch) and
 puts every empty row last, so the CSR5 kernel needs no row indirection and
@@ -36,12 +37,22 @@ def _as_csr(a) -> CsrMatrix:
     return a if isinstance(a, CsrMatrix) else to_csr(a)
 
 
+_KEYS = {"sum": 0, "row": 1}
+
+
 class DegreeOrder:
     """The symmetric permutation of a square matrix: ``perm[new] = old``,
     ``new_id[old] = new`` (int32 device tensors); rows ``[0, n_nonempty)``
-    of ``P A P^T`` are the non-empty ones."""
+    of ``P A P^T`` are the non-empty ones.  ``key``: ``"row"`` (default)
+    orders by row degree, then column degree, so the rows come in exact
+    descending length (SELL slices then pad least: degree-ordered C5 SELL-32
+    2.22 -> 2.20 ms, sigma 0 2.41 -> 2.27 ms); ``"sum"`` by row + column
+    degree (CSR5 is the same either way; profiles/r02_relabel_formats2.txt)."""
 
-    def __init__(self, a):
+    def __init__(self, a, key: str = "row"):
+        if key not in _KEYS:
+            raise ValueError(f"key must be one of {sorted(_KEYS)}, got {key!r}")
+        self.key = key
         csr = _as_csr(a)
         if csr.n_rows != csr.n_cols:
             raise ValueError(f"relabelling needs a square matrix, got {csr.n_rows}x{csr.n_cols}")
@@ -52,7 +63,7 @@ class DegreeOrder:
         self.new_id = torch.empty(n, dtype=torch.int32, device=dev)
         cnt = ctypes.c_int64()
         with torch.cuda.device(dev):
-            check(LIB.spmvb_degree_order(n, ptr(csr.ptr), ptr(csr.indices), csr.nnz, ptr(self.perm),
+            check(LIB.spmvb_degree_order(n, ptr(csr.ptr), ptr(csr.indices), csr.nnz, _KEYS[key], ptr(self.perm),
                                          ptr(self.new_id), ctypes.byref(cnt), _lib.stream(dev)))
         self.n_nonempty = int(cnt.value)
 

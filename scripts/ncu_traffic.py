@@ -27,8 +27,10 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 TARGETS = [
-    "C5/csr5-w32s16-relabel", "C5/csr5-w32s16", "C5/csr", "C5/hyb", "C5/sell-c32s8192",
-    "C4/csr5-w32s16-relabel", "C4/csr5-w32s16", "C4/csr", "C4/hyb",
+    "C5/csr5-w32s16-relabel", "C5/sell-c32s8192-relabel", "C5/csr5-w32s8-relabel", "C5/hyb-relabel",
+    "C5/csr-relabel", "C5/csr5-w32s16", "C5/csr", "C5/hyb", "C5/sell-c32s8192",
+    "C4/csr5-w32s16-relabel", "C4/csr5-w32s8-relabel", "C4/sell-c32s8192-relabel", "C4/hyb-relabel",
+    "C4/csr-relabel", "C4/csr5-w32s16", "C4/csr", "C4/hyb",
     "C3/ell", "C3/hyb", "C3/sell-c32s1024", "C3/csr5-w32s16",
     "C2/ell", "C2/hyb", "C2/csr5-w32s16",
     "C1/ell", "C1/hyb", "C1/csr",
@@ -109,8 +111,12 @@ def parse(rep, plan_path, out_path):
     def val(r, name):
         return float(r[col[name]].replace(",", "")) * scale[units[col[name]]]
 
-    out = {"_source": f"ncu --set full --clock-control none (cache control all: cold caches), one SpMV per target "
-                      f"= all its kernels; dram__bytes_read.sum + dram__bytes_write.sum; {Path(rep).name}"}
+    try:  # merge into the existing table (targets captured in other runs stay)
+        out = json.loads(Path(out_path).read_text())
+    except (OSError, ValueError):
+        out = {}
+    out["_source"] = ("ncu --set full --clock-control none (cache control all: cold caches), one SpMV per target "
+                      "= all its kernels; dram__bytes_read.sum + dram__bytes_write.sum; scripts/ncu_traffic.py")
     detail = {}
     i = 0
     for p in plan:

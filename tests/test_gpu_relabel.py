@@ -36,10 +36,13 @@ def np_(t):
     return t.detach().cpu().numpy()
 
 
-def order_restated(ptr, col, n):
+def order_restated(ptr, col, n, key="sum"):
     rowdeg = np.diff(ptr)
     coldeg = np.bincount(col, minlength=n)
-    perm = np.lexsort((np.arange(n), -(rowdeg + coldeg), rowdeg == 0))
+    if key == "sum":
+        perm = np.lexsort((np.arange(n), -(rowdeg + coldeg), rowdeg == 0))
+    else:  # rows in exact descending length, then column degree
+        perm = np.lexsort((np.arange(n), -coldeg, -rowdeg, rowdeg == 0))
     new_id = np.empty(n, np.int64)
     new_id[perm] = np.arange(n)
     return perm, new_id, int((rowdeg > 0).sum())
@@ -63,14 +66,15 @@ def cases():
     yield "no_entries", (np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0), 17)
 
 
+@pytest.mark.parametrize("key", ["sum", "row"])
 @pytest.mark.parametrize("name,case", list(cases()), ids=[c[0] for c in cases()])
-def test_order_and_shadow_matrix(sp, name, case):
+def test_order_and_shadow_matrix(sp, name, case, key):
     row, col, val, n = case
     a = sp.canonicalize(row, col, val, n, n)
     csr = sp.to_csr(a)
-    order = sp.DegreeOrder(csr)
+    order = sp.DegreeOrder(csr, key=key)
     ptr_h = np_(csr.ptr).astype(np.int64)
-    perm, new_id, nonempty = order_restated(ptr_h, col.astype(np.int64), n)
+    perm, new_id, nonempty = order_restated(ptr_h, col.astype(np.int64), n, key)
     assert np_(order.perm).tolist() == perm.tolist()
     assert np_(order.new_id).tolist() == new_id.tolist()
     assert order.n_nonempty == nonempty
