@@ -141,25 +141,33 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
   }
 }
 
-// Thread per (wide slice, row): the row's pieces in order.
+// Warp per (wide slice, row): lane k adds pieces k, k+32, ... in order, then
+// the xor butterfly (a fixed order: deterministic).  A thread per row adding
+// its pieces one after another was a chain of dependent loads as long as the
+// row's piece count (~400 for a degree-ordered C5 hub row: 41 us).
 __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
                                   const int32_t* __restrict__ first_piece, int64_t n_pieces,
                                   const double* __restrict__ part, const int32_t* __restrict__ perm,
                                   double* __restrict__ y, const double* __restrict__ scale_p) {
   pdl_wait();
   const double sc = load_scale(scale_p);
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n_wide * c;
-       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = warp; q < n_wide * c; q += nwarps) {
     const int64_t i = q / c;
     const int l = static_cast<int>(q - i * c);
     const int64_t sl = wide[i];
     if (l >= sell_rows(sl, c, n_rows)) continue;
     const int32_t p0 = first_piece[i], p1 = i + 1 < n_wide ? first_piece[i + 1] : static_cast<int32_t>(n_pieces);
     double sum = 0.0;
-    for (int32_t pc = p0; pc < p1; ++pc) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
-    const int64_t p = sl * c + l;
-    const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
-    y[r] = scale_p ? sc * sum : sum;
+    for (int32_t pc = p0 + lane; pc < p1; pc += 32) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
+    sum = warp_sum(sum);
+    if (lane == 0) {
+      const int64_t p = sl * c + l;
+      const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
+      y[r] = scale_p ? sc * sum : sum;
+    }
   }
 }
 
@@ -260,7 +268,8 @@ extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths,
       launch_pdl(k_sell_wide_part, dim3(grid_for(n_pieces, 1, 148 * 16)), dim3(256), 0, s, n_rows, c, wide, n_wide,
                  first_piece, n_pieces, widths, slice_off, idx, val, x, part.get());
       SPMVB_LAUNCHED("k_sell_wide_part");
-      launch_pdl(k_sell_wide_final, dim3(grid_for(n_wide * c, 256)), dim3(256), 0, s, n_rows, c, wide, n_wide,
+      launch_pdl(k_sell_wide_final, dim3(grid_for(n_wide * c * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows, c, wide,
+                 n_wide,
                  first_piece, n_pieces, part.get(), perm, y, scale);
       SPMVB_LAUNCHED("k_sell_wide_final");
     }
