@@ -293,10 +293,13 @@ int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* 
 int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int64_t wide_cols, int32_t* wide_out,
                          int64_t* n_wide, int64_t* max_narrow_width, int32_t* first_piece_out, int64_t* n_pieces,
                          void* stream);
+/* tail_from (n_rows = none): the caller's promise that every permuted row
+ * p >= tail_from is empty with perm[p] == p (a degree-ordered matrix's empty
+ * tail); those rows get y = 0 without any slice or perm lookups. */
 int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                     const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
-                    const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols, int64_t max_narrow_width,
-                    const double* x, double* y, const double* scale, void* stream);
+                    const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols, int64_t tail_from,
+                    int64_t max_narrow_width, const double* x, double* y, const double* scale, void* stream);
 
 /* ||y||^2 over n entries into *out (device), deterministic two-level sum.
  * Used by power iteration. */

@@ -39,12 +39,17 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? (SPMVB_SELL_
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p,
-                            int64_t wide_cols) {
+                            int64_t wide_cols, int64_t tail_from) {
   pdl_wait();
   const double s = load_scale(scale_p);
+  const double zero = scale_p ? s * 0.0 : 0.0;  // an empty row's result
   const int32_t c32 = static_cast<int32_t>(c);  // n_rows < 2^31: 32-bit slice arithmetic
   for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n_rows;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (p >= tail_from) {  // the empty tail (perm is the identity there): plain coalesced stores
+      y[p] = zero;
+      continue;
+    }
     const int32_t p32 = static_cast<int32_t>(p);
     const int32_t sl = p32 / c32, local = p32 - sl * c32;
     const int64_t rows_s = (static_cast<int64_t>(sl) + 1) * c <= n_rows ? c : n_rows - static_cast<int64_t>(sl) * c;
@@ -247,12 +252,13 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
                                int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
-                               int64_t max_narrow_width, const double* x, double* y, const double* scale,
-                               void* stream) {
+                               int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
+                               const double* scale, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
     if (wide_cols <= 0) wide_cols = SPMVB_SELL_WIDE_COLS;
+    if (tail_from < 0 || tail_from > n_rows) tail_from = n_rows;
     // c < 8: slot loads through L1 (the other half of each index sector is
     // the next slot's); rows of 8 or more slots: next four slots prefetched
     const unsigned g = grid_for(n_rows, 256);
@@ -260,7 +266,8 @@ extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths,
     // 36.9 / 50.2 us L2-flushed against mode 1)
     const bool wide_rows = max_narrow_width >= 8 || max_narrow_width < 0;
     auto kern = c < 8 ? (wide_rows ? k_spmv_sell<3> : k_spmv_sell<1>) : (wide_rows ? k_spmv_sell<2> : k_spmv_sell<0>);
-    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale, wide_cols);
+    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale, wide_cols,
+               tail_from);
     SPMVB_LAUNCHED("k_spmv_sell");
     if (n_wide > 0) {
       if (!first_piece || n_pieces < n_wide) fail(SPMVB_INVALID_ARG, "wide-slice piece plan missing");

@@ -305,8 +305,23 @@ class SellMatrix:
                 check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), wide_cols, ptr(lst),
                                                ctypes.byref(cnt), ctypes.byref(mx), ptr(first),
                                                ctypes.byref(npieces), _lib.stream(self.device)))
-            self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value), wide_cols)
+            self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value), wide_cols,
+                          self._empty_tail())
         return self._wide
+
+    def _empty_tail(self) -> int:
+        """First permuted row of the trailing all-empty slices if perm is the
+        identity from there on (a degree-ordered matrix), else n_rows."""
+        n = self.n_rows
+        if n == 0:
+            return 0
+        nz = torch.nonzero(self.widths > 0)
+        tail = min((int(nz[-1].item()) + 1) * self.c, n) if nz.numel() else 0
+        if tail < n and self.sigma > 0:
+            ident = torch.arange(tail, n, dtype=self.perm.dtype, device=self.device)
+            if not torch.equal(self.perm[tail:], ident):
+                return n
+        return tail
 
     def _host_layout(self):
         if self._host is None:

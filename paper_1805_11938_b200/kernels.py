@@ -275,11 +275,11 @@ def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
 
 
 def _args_sell(m: SellMatrix, xd, y, sp, scratch):
-    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols = m.wide_plan()
+    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from = m.wide_plan()
     perm = m.perm if m.sigma > 0 else None
     return "spmvb_spmv_sell", (m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices),
-                               ptr(m.flat_data), ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, max_narrow,
-                               ptr(xd), ptr(y), sp)
+                               ptr(m.flat_data), ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, tail_from,
+                               max_narrow, ptr(xd), ptr(y), sp)
 
 
 def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):

@@ -174,3 +174,27 @@ def test_relabelled_spmv_at_c4(sp):
     y_back = rm.order.to_old(yp)
     bound_o = sp.dense_spmv_oracle(sp.canonicalize(a.row, a.col, a.data.abs(), n, n), x.abs())
     assert bool(((y_back - y_plain).abs() <= 2 * TOL * bound_o).all())
+
+
+@pytest.mark.parametrize("c,sigma", [(32, 0), (32, 256), (4, 0), (4, 8)])
+def test_relabelled_sell_empty_tail(sp, c, sigma):
+    """SELL of a degree-ordered matrix: its trailing all-empty slices are
+    zeroed without slice/perm lookups (spmvb_spmv_sell tail_from); y is
+    bit-identical to the reference SELL recurrence (port.spmv_sell) and
+    stale values in the tail are overwritten."""
+    row, col, val, n = rmat_host(12, 8, 13)
+    a = sp.canonicalize(row, col, val, n, n)
+    order = sp.DegreeOrder(a)
+    shadow = order.matrix(a)
+    m = sp.to_sell(shadow, c, sigma)
+    tail = m.wide_plan()[6]
+    assert tail < n  # the empty rows form a tail the kernel can skip
+    sptr = np_(shadow.ptr).astype(np.int64)
+    so = port.to_sell(sptr, np_(shadow.indices).astype(np.int64), np_(shadow.data), n, c, sigma)
+    x = synth_ref.uniform(n, 21)
+    y = torch.full((n,), 7.0, dtype=torch.float64, device="cuda")
+    sp.spmv("sell", m, torch.from_numpy(x).cuda(), out=y)
+    want = port.spmv_sell(so, n, x)
+    if int(so.widths.max()) <= 256:
+        assert np_(y).tobytes() == want.tobytes()
+    assert np.all(np_(y)[order.n_nonempty:] == 0.0)
