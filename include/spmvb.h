@@ -326,6 +326,24 @@ int spmvb_column_set(const int32_t* col, int64_t nnz, int64_t n_cols, int32_t* c
 int spmvb_gather_f64(const double* src, int64_t base, const int32_t* idx, int64_t n, double* dst, void* stream);
 int spmvb_scatter_f64(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream);
 
+/* Row-block power iteration over a caller-owned NCCL communicator (SURVEY
+ * §8(b) dist_{init,spmv_iter,destroy}; the torch.distributed version is
+ * dist.PowerIteration).  spmvb_dist_init: nccl_comm is an ncclComm_t of
+ * `world` ranks (this one is `rank`); bounds: world + 1 host row boundaries
+ * (e.g. nnz-balanced).  spmvb_dist_step, on `stream`: local_spmv(ctx, x,
+ * x_next + bounds[rank], scale, stream) must write this rank's rows
+ * scale * A_p x (any spmvb_spmv_* call; return its status); then
+ * *sumsq = ||y||^2 over all ranks (NCCL all-reduce), x_next gathered from
+ * every rank (grouped NCCL send/recv with per-rank counts) and *scale =
+ * 1/||y|| (device scalars), so x_{k+1} = x_next * scale.  NCCL is resolved
+ * at run time from the libnccl.so.2 loaded in the process. */
+typedef struct spmvb_dist spmvb_dist;
+typedef int (*spmvb_local_spmv_fn)(void* ctx, const double* x, double* y_local, const double* scale, void* stream);
+int spmvb_dist_init(void* nccl_comm, int rank, int world, const int64_t* bounds, spmvb_dist** out);
+int spmvb_dist_step(spmvb_dist* d, spmvb_local_spmv_fn local_spmv, void* ctx, const double* x, double* x_next,
+                    double* sumsq, double* scale, void* stream);
+int spmvb_dist_destroy(spmvb_dist* d);
+
 /* Degree-ordered symmetric relabelling (relabel.cu): an internal shadow
  * layout P A P^T of a square n x n CSR for iterative SpMV (power iteration
  * on R-MAT: CSR5 SpMV ~13 % faster at scale 25); the reference's arrays are

@@ -113,6 +113,9 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_degree_order": (c_int, [c_i64, vp, vp, c_i64, c_int, vp, vp, P_i64, vp]),
     "spmvb_relabel_csr": (c_int, [c_i64, vp, vp, vp, c_i64, vp, vp, vp, vp, vp]),
     "spmvb_push_rows": (c_int, [vp, c_i64, vp, c_int, c_i64, vp]),
+    "spmvb_dist_init": (c_int, [vp, c_int, c_int, vp, P_vp]),
+    "spmvb_dist_step": (c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvb_dist_destroy": (c_int, [vp]),
     "spmvb_sum_inv_sqrt": (c_int, [vp, c_int, vp, vp, vp]),
     "spmvb_gather_probe_threads": (c_i64, []),
     "spmvb_gather_probe": (c_int, [vp, vp, c_i64, vp, vp]),

@@ -47,7 +47,8 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import CsrMatrix
 
-__all__ = ["nnz_balanced_bounds", "cost_balanced_bounds", "row_block", "PowerIteration", "GpuOps"]
+__all__ = ["nnz_balanced_bounds", "cost_balanced_bounds", "row_block", "PowerIteration", "NativePowerIteration",
+           "GpuOps"]
 
 
 def nnz_balanced_bounds(row_ptr, parts: int) -> np.ndarray:
@@ -623,3 +624,60 @@ class PowerIteration:
         """||A x_k|| for the current normalised iterate (1/scale)."""
         s = float(self.scale.item())
         return 1.0 / s if s > 0 else math.nan
+
+
+class NativePowerIteration:
+    """The row-block power iteration through the C ABI's ``spmvb_dist_*``
+    (a caller-owned NCCL communicator), for parity with what a
+    non-Python caller gets.  ``local_op`` binds the shard's SpMV
+    (``kernels.SpmvOperator`` or ``relabel.RelabelledMatrix``);
+    ``comm_ptr`` is the ``ncclComm_t`` address (from torch:
+    ``group._get_backend(device)._comm_ptr()``).  Same step as
+    ``PowerIteration``'s all-gatherv path, bit for bit."""
+
+    _CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p)
+
+    def __init__(self, local_op, bounds, rank: int, world: int, device: torch.device, x0: torch.Tensor,
+                 comm_ptr: int):
+        self.bounds = [int(b) for b in bounds]
+        self.rank, self.world, self.device = rank, world, device
+        n = self.bounds[-1]
+        lo, hi = self.bounds[rank], self.bounds[rank + 1]
+        self.x = x0.to(device=device, dtype=torch.float64).clone()
+        self.x_next = torch.empty(n, dtype=torch.float64, device=device)
+        self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
+        self.scale = torch.ones(1, dtype=torch.float64, device=device)
+        # the SpMV of each parity, bound once; the callback picks it by x
+        self._calls = {int(a.data_ptr()): local_op.bind(a, b[lo:hi], self.scale)
+                       for a, b in ((self.x, self.x_next), (self.x_next, self.x))}
+
+        def local(ctx, x, y, scale, stream):
+            try:
+                self._calls[int(x)]()
+                return 0
+            except Exception:  # reported through the status code
+                return _lib.SPMVB_INTERNAL
+
+        self._cb = self._CB(local)  # keep the callback alive with the object
+        b = (ctypes.c_int64 * len(self.bounds))(*self.bounds)
+        h = ctypes.c_void_p()
+        check(LIB.spmvb_dist_init(ctypes.c_void_p(comm_ptr), rank, world, b, ctypes.byref(h)))
+        self._h = h
+
+    def step(self) -> None:
+        with torch.cuda.device(self.device):
+            check(LIB.spmvb_dist_step(self._h, ctypes.cast(self._cb, ctypes.c_void_p), None, ptr(self.x),
+                                      ptr(self.x_next), ptr(self.sumsq), ptr(self.scale), _lib.stream(self.device)))
+        self.x, self.x_next = self.x_next, self.x
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            check(LIB.spmvb_dist_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -3,8 +3,8 @@ round-end boxes of this project have one).  The three exchanges of the
 row-block power iteration (dist.py) -- the NCCL all-gatherv overlapped with
 CSR5 tile ranges, the sparse exchange and the peer-memory exchange (p2p, our
 kernels over NVLink through symmetric memory: fused SpMV + peer store, and
-the separate push kernel) -- must give the same iterate as the serial
-power iteration of oracle/port.py (the reference CSR algorithm,
+the separate push kernel) and the C ABI's spmvb_dist_* step -- must give
+the same iterate as the serial power iteration of oracle/port.py (the reference CSR algorithm,
 kernels.py:76-95, partitioned as kernels.py:61-66 does per task)."""
 
 from __future__ import annotations
@@ -67,6 +67,18 @@ def _worker(rank, world, port_no, out, exchange, fused):
             sp.spmv_csr5_push(m, x, o, peers, off, scale=s, carry=carry)
 
     x0 = synth_ref.uniform(n, 7)
+    if exchange == "native":  # the C ABI's spmvb_dist_* over torch's NCCL communicator
+        comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
+        pi = spdist.NativePowerIteration(sp.SpmvOperator("csr5", m), bounds, rank, world, dev,
+                                         torch.from_numpy(x0).to(dev), comm)
+        for _ in range(STEPS):
+            pi.step()
+        torch.cuda.synchronize()
+        out[rank] = (pi.x.cpu().numpy().copy(), float(pi.scale.item()))
+        pi.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     pi = spdist.PowerIteration(sp.SpmvOperator("csr5", m), bounds, rank, world, dev, torch.from_numpy(x0).to(dev),
                                exchange=exchange, local_cols=shard.indices if exchange == "sparse" else None,
                                local_ranges=[(a, b) for a, b, _, _ in plan], local_spmv_range=range_fn,
@@ -93,7 +105,7 @@ def _serial():
 
 
 @pytest.mark.parametrize("exchange,fused", [("allgatherv", False), ("sparse", False), ("p2p", True),
-                                            ("p2p", False)])
+                                            ("p2p", False), ("native", False)])
 def test_two_gpu_exchanges_match_serial(exchange, fused):
     out = mp.get_context("spawn").Manager().dict()
     mp.spawn(_worker, args=(2, _free_port(), out, exchange, fused), nprocs=2, join=True)
