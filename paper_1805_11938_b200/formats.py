@@ -281,12 +281,19 @@ class SellMatrix:
         header's SPMVB_SELL_WIDE_COLS) unless the matrix is big enough for
         longer per-thread rows to hide behind the rest of the grid: about
         twice the cells per resident thread, rounded up to a power of two,
-        at most 4096 (degree-ordered C5: 2.20 -> 2.09 ms at 4096; C4 stays
-        at 256, where 1024 would serialise it: 135 -> 222 us;
+        at most 4096, and only if the wide slices are all in the first
+        quarter of the grid (degree-ordered C5: 2.20 -> 2.09 ms at 4096; C4
+        stays at 256, where 1024 would serialise it: 135 -> 222 us;
         profiles/r02_sell_ab2.txt)."""
+        w = 256
+        wide = torch.nonzero(self.widths > w)
+        # only when the wide slices come first (rows in descending length, a
+        # degree-ordered matrix): their long threads then start with the grid
+        # instead of trailing it (reference-layout C5 would lose 3.23 -> 3.43 ms)
+        if wide.numel() == 0 or int(wide[-1].item()) >= self.n_slices // 4:
+            return w
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         per_thread = self.total_cells / max(sms * 2048, 1)
-        w = 256
         while w < 4096 and w < 2 * per_thread:
             w *= 2
         return w
