@@ -265,12 +265,16 @@ def variant_label(tag, kw):
 
 # Formats timed on the degree-ordered shadow layout (R-MAT power iteration);
 # the fastest carries the timed run
+# (the shadow layout already has its rows in descending length, so SELL
+# needs no sorting window: sigma 0 gives the same slices without the
+# permutation, and slice-granular row ranges for the multi-GPU overlap;
+# profiles/r02_relabel_formats3.txt: C5 1.98 ms vs 2.04 ms with sigma 8192)
 RUN_CANDIDATES = [
     ("csr", {}),
     ("csr5", dict(omega=32, sigma=16)),
     ("csr5", dict(omega=32, sigma=8)),
     ("hyb", dict(max_cells=1 << 34)),
-    ("sell", dict(sell_c=32, sell_sigma=32 * 256, max_cells=1 << 34)),
+    ("sell", dict(sell_c=32, sell_sigma=0, max_cells=1 << 34)),
 ]
 
 # C1-C4 (the `configs` block of the default run): every format at the
@@ -667,6 +671,13 @@ def run_ours(args):
     # overlap (N > 1, CSR5 shards): row-aligned tile ranges, light rows first,
     # each range's rows sent to the peers while the next range computes
     ranges, range_fn = None, None
+    if world > 1 and tag == "sell" and args.overlap_ranges > 1:
+        # SELL: slice ranges aligned to the sorting windows, last (light) first
+        splan = m.range_plan(args.overlap_ranges)[::-1]
+        ranges = [(r_[6], r_[7]) for r_ in splan]
+
+        def range_fn(k, xv, out, scale):
+            sp.spmv_sell_range(m, xv, out, splan[k], scale=scale)
     if world > 1 and tag == "csr5" and args.overlap_ranges > 1:
         tb, rb = m.range_plan(args.overlap_ranges)
         k_all = len(tb) - 1
@@ -940,7 +951,7 @@ def main():
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--overlap-ranges", type=int, default=4,
-                    help="N > 1, CSR5 shards: row ranges whose all-gatherv overlaps the remaining local SpMV")
+                    help="N > 1, CSR5 / SELL shards: row ranges whose all-gatherv overlaps the remaining local SpMV")
     ap.add_argument("--balance", choices=["nnz", "cost"], default="nnz",
                     help="N > 1 row blocks: nnz-balanced (the config's) or nnz + 1.5 rows (see dist.cost_balanced_bounds)")
     ap.add_argument("--compare-p2p", action="store_true",

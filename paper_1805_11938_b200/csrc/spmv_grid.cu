@@ -39,12 +39,12 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? (SPMVB_SELL_
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p,
-                            int64_t wide_cols, int64_t tail_from) {
+                            int64_t wide_cols, int64_t tail_from, int64_t p_begin, int64_t p_end) {
   pdl_wait();
   const double s = load_scale(scale_p);
   const double zero = scale_p ? s * 0.0 : 0.0;  // an empty row's result
   const int32_t c32 = static_cast<int32_t>(c);  // n_rows < 2^31: 32-bit slice arithmetic
-  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n_rows;
+  for (int64_t p = p_begin + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < p_end;
        p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (p >= tail_from) {  // the empty tail (perm is the identity there): plain coalesced stores
       y[p] = zero;
@@ -92,11 +92,12 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
                                                         const int64_t* __restrict__ widths,
                                                         const int64_t* __restrict__ slice_off,
                                                         const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                                        const double* __restrict__ x, double* __restrict__ part) {
+                                                        const double* __restrict__ x, double* __restrict__ part,
+                                                        int32_t pc_begin, int32_t pc_end) {
   pdl_wait();
   __shared__ double red[256];
   const int t = threadIdx.x;
-  for (int32_t item = blockIdx.x; item < n_pieces; item += gridDim.x) {
+  for (int32_t item = pc_begin + blockIdx.x; item < pc_end; item += gridDim.x) {
     // wide slice holding this piece: last i with first_piece[i] <= item
     int64_t lo = 0, hi = n_wide - 1;
     while (lo < hi) {
@@ -153,13 +154,14 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
 __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
                                   const int32_t* __restrict__ first_piece, int64_t n_pieces,
                                   const double* __restrict__ part, const int32_t* __restrict__ perm,
-                                  double* __restrict__ y, const double* __restrict__ scale_p) {
+                                  double* __restrict__ y, const double* __restrict__ scale_p, int64_t i_begin,
+                                  int64_t i_end) {
   pdl_wait();
   const double sc = load_scale(scale_p);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t q = warp; q < n_wide * c; q += nwarps) {
+  for (int64_t q = i_begin * c + warp; q < i_end * c; q += nwarps) {
     const int64_t i = q / c;
     const int l = static_cast<int>(q - i * c);
     const int64_t sl = wide[i];
@@ -249,37 +251,74 @@ extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, con
   });
 }
 
+namespace {
+
+// Slices [s_begin, s_end) of a SELL SpMV: the per-row kernel over their rows,
+// the pieces [pc_begin, pc_end) of the wide slices [i_begin, i_end) among
+// them, and those wide rows' sums.
+void sell_launch(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off, const int32_t* perm,
+                 const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
+                 const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols, int64_t tail_from,
+                 int64_t max_narrow_width, const double* x, double* y, const double* scale, int64_t s_begin,
+                 int64_t s_end, int64_t i_begin, int64_t i_end, int64_t pc_begin, int64_t pc_end, cudaStream_t s) {
+  if (wide_cols <= 0) wide_cols = SPMVB_SELL_WIDE_COLS;
+  if (tail_from < 0 || tail_from > n_rows) tail_from = n_rows;
+  const int64_t p_begin = s_begin * c, p_end = s_end * c < n_rows ? s_end * c : n_rows;
+  if (p_end > p_begin) {
+    // c < 8: slot loads through L1 (the other half of each index sector is
+    // the next slot's); rows of 8 or more slots: next four slots prefetched
+    // (C2 / C3 with the reference default C = 4: mode 3 41.0 / 63.5 ->
+    // 36.9 / 50.2 us L2-flushed against mode 1)
+    const unsigned g = grid_for(p_end - p_begin, 256);
+    const bool wide_rows = max_narrow_width >= 8 || max_narrow_width < 0;
+    auto kern = c < 8 ? (wide_rows ? k_spmv_sell<3> : k_spmv_sell<1>) : (wide_rows ? k_spmv_sell<2> : k_spmv_sell<0>);
+    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale, wide_cols,
+               tail_from, p_begin, p_end);
+    SPMVB_LAUNCHED("k_spmv_sell");
+  }
+  if (i_end > i_begin) {
+    if (!first_piece || n_pieces < n_wide || pc_end <= pc_begin) fail(SPMVB_INVALID_ARG, "wide-slice piece plan missing");
+    DevBuf<double> part(static_cast<size_t>(n_pieces) * SELL_PART_STRIDE, s);
+    launch_pdl(k_sell_wide_part, dim3(grid_for(pc_end - pc_begin, 1, 148 * 16)), dim3(256), 0, s, n_rows, c, wide,
+               n_wide, first_piece, n_pieces, widths, slice_off, idx, val, x, part.get(),
+               static_cast<int32_t>(pc_begin), static_cast<int32_t>(pc_end));
+    SPMVB_LAUNCHED("k_sell_wide_part");
+    launch_pdl(k_sell_wide_final, dim3(grid_for((i_end - i_begin) * c * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows,
+               c, wide, n_wide, first_piece, n_pieces, part.get(), perm, y, scale, i_begin, i_end);
+    SPMVB_LAUNCHED("k_sell_wide_final");
+  }
+}
+
+}  // namespace
+
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
                                int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
                                int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
                                const double* scale, void* stream) {
   return guard([&] {
-    cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
-    if (wide_cols <= 0) wide_cols = SPMVB_SELL_WIDE_COLS;
-    if (tail_from < 0 || tail_from > n_rows) tail_from = n_rows;
-    // c < 8: slot loads through L1 (the other half of each index sector is
-    // the next slot's); rows of 8 or more slots: next four slots prefetched
-    const unsigned g = grid_for(n_rows, 256);
-    // (C2 / C3 with the reference default C = 4: mode 3 41.0 / 63.5 ->
-    // 36.9 / 50.2 us L2-flushed against mode 1)
-    const bool wide_rows = max_narrow_width >= 8 || max_narrow_width < 0;
-    auto kern = c < 8 ? (wide_rows ? k_spmv_sell<3> : k_spmv_sell<1>) : (wide_rows ? k_spmv_sell<2> : k_spmv_sell<0>);
-    launch_pdl(kern, dim3(g), dim3(256), 0, s, n_rows, c, widths, slice_off, perm, idx, val, x, y, scale, wide_cols,
-               tail_from);
-    SPMVB_LAUNCHED("k_spmv_sell");
-    if (n_wide > 0) {
-      if (!first_piece || n_pieces < n_wide) fail(SPMVB_INVALID_ARG, "wide-slice piece plan missing");
-      DevBuf<double> part(static_cast<size_t>(n_pieces) * SELL_PART_STRIDE, s);
-      launch_pdl(k_sell_wide_part, dim3(grid_for(n_pieces, 1, 148 * 16)), dim3(256), 0, s, n_rows, c, wide, n_wide,
-                 first_piece, n_pieces, widths, slice_off, idx, val, x, part.get());
-      SPMVB_LAUNCHED("k_sell_wide_part");
-      launch_pdl(k_sell_wide_final, dim3(grid_for(n_wide * c * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows, c, wide,
-                 n_wide,
-                 first_piece, n_pieces, part.get(), perm, y, scale);
-      SPMVB_LAUNCHED("k_sell_wide_final");
-    }
+    sell_launch(n_rows, c, widths, slice_off, perm, idx, val, wide, n_wide, first_piece, n_pieces, wide_cols,
+                tail_from, max_narrow_width, x, y, scale, 0, (n_rows + c - 1) / c, 0, n_wide, 0, n_pieces,
+                as_stream(stream));
+  });
+}
+
+extern "C" int spmvb_spmv_sell_range(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
+                                     const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
+                                     int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
+                                     int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
+                                     const double* scale, int64_t s_begin, int64_t s_end, int64_t i_begin,
+                                     int64_t i_end, int64_t pc_begin, int64_t pc_end, void* stream) {
+  return guard([&] {
+    if (n_rows <= 0) return;
+    const int64_t n_slices = (n_rows + c - 1) / c;
+    if (s_begin < 0 || s_end < s_begin || s_end > n_slices || i_begin < 0 || i_end < i_begin || i_end > n_wide ||
+        pc_begin < 0 || pc_end < pc_begin || pc_end > n_pieces)
+      fail(SPMVB_INVALID_ARG, "slice / wide-slice / piece range out of bounds");
+    sell_launch(n_rows, c, widths, slice_off, perm, idx, val, wide, n_wide, first_piece, n_pieces, wide_cols,
+                tail_from, max_narrow_width, x, y, scale, s_begin, s_end, i_begin, i_end, pc_begin, pc_end,
+                as_stream(stream));
   });
 }
 

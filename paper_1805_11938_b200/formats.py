@@ -274,6 +274,7 @@ class SellMatrix:
         self.row_nnz_perm = row_nnz_perm
         self._host = None
         self._wide = None
+        self._ranges = {}
 
     def wide_cols(self) -> int:
         """Slices up to this width are summed one thread per row (sequential,
@@ -315,6 +316,38 @@ class SellMatrix:
             self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value), wide_cols,
                           self._empty_tail())
         return self._wide
+
+    def range_plan(self, k: int):
+        """About ``k`` slice ranges of roughly equal cells, aligned to the
+        sigma sorting windows (so each range's rows are one contiguous block
+        of y): a list of (s_begin, s_end, i_begin, i_end, pc_begin, pc_end,
+        row_begin, row_end) for ``kernels.spmv_sell_range``; cached."""
+        key = int(k)
+        if key in self._ranges:
+            return self._ranges[key]
+        wide, n_wide, _, first, n_pieces = self.wide_plan()[:5]
+        S = self.n_slices
+        align = max(self.sigma // self.c, 1) if self.sigma > 0 else 1
+        off = self.slice_off.cpu().numpy()
+        total = int(off[-1]) if S else 0
+        cuts = [0]
+        for j in range(1, max(key, 1)):
+            sj = int(np.searchsorted(off, total * j / key, side="left"))
+            sj = min((sj // align) * align, S)
+            if sj > cuts[-1]:
+                cuts.append(sj)
+        if S > cuts[-1]:
+            cuts.append(S)
+        wl = wide[:n_wide].cpu().numpy() if n_wide else np.empty(0, np.int32)
+        fp = first[:n_wide].cpu().numpy() if n_wide else np.empty(0, np.int32)
+        plan = []
+        for s0, s1 in zip(cuts[:-1], cuts[1:]):
+            i0, i1 = int(np.searchsorted(wl, s0)), int(np.searchsorted(wl, s1))
+            pc0 = int(fp[i0]) if i0 < n_wide else n_pieces
+            pc1 = int(fp[i1]) if i1 < n_wide else n_pieces
+            plan.append((s0, s1, i0, i1, pc0, pc1, s0 * self.c, min(s1 * self.c, self.n_rows)))
+        self._ranges[key] = plan
+        return plan
 
     def _empty_tail(self) -> int:
         """First permuted row of the trailing all-empty slices if perm is the

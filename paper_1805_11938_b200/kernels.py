@@ -25,8 +25,8 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import Csr5Matrix, CsrMatrix, EllMatrix, FormatMatrix, FormatTag, HybMatrix, SellMatrix
 
-__all__ = ["BoundCall", "SpmvOperator", "bind", "plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push", "spmv_csr5_tiles", "spmv_ell",
-           "spmv_hyb", "spmv_many", "spmv_sell"]
+__all__ = ["BoundCall", "SpmvOperator", "bind", "plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push",
+           "spmv_csr5_tiles", "spmv_ell", "spmv_hyb", "spmv_many", "spmv_sell", "spmv_sell_range"]
 
 
 def plan_row_blocks(n_rows: int, workers: int) -> list[tuple[int, int]]:
@@ -291,6 +291,27 @@ def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
         check(getattr(LIB, name)(*args, s))
 
     return _run(m, x, out, scale, launch)
+
+
+def spmv_sell_range(m: SellMatrix, x: torch.Tensor, out: torch.Tensor, r, *, scale=None) -> torch.Tensor:
+    """One slice range of a SELL SpMV on device buffers (spmvb_spmv_sell_range);
+    ``r`` is an entry of ``m.range_plan(k)``.  Over all of a plan's ranges, in
+    any order, this equals ``spmv_sell(m, x, out=out)`` bit for bit; the
+    multi-GPU power iteration sends each range's rows (r[6]:r[7] of y) while
+    the next one computes."""
+    xd = x.reshape(-1)
+    if not xd.is_cuda or xd.dtype != torch.float64 or xd.numel() != m.n_cols:
+        raise ValueError(f"x must be a float64 CUDA tensor of length {m.n_cols}")
+    y = _out(m, out)
+    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from = m.wide_plan()
+    perm = m.perm if m.sigma > 0 else None
+    s0, s1, i0, i1, pc0, pc1 = (int(v) for v in r[:6])
+    with torch.cuda.device(m.device):
+        check(LIB.spmvb_spmv_sell_range(
+            m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
+            ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, tail_from, max_narrow, ptr(xd.contiguous()),
+            ptr(y), ptr(scale) if scale is not None else None, s0, s1, i0, i1, pc0, pc1, _lib.stream(m.device)))
+    return y
 
 
 def _args_hyb(m: HybMatrix, xd, y, sp, scratch):

@@ -27,9 +27,9 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 TARGETS = [
-    "C5/csr5-w32s16-relabel", "C5/sell-c32s8192-relabel", "C5/csr5-w32s8-relabel", "C5/hyb-relabel",
+    "C5/csr5-w32s16-relabel", "C5/sell-c32s0-relabel", "C5/sell-c32s8192-relabel", "C5/csr5-w32s8-relabel", "C5/hyb-relabel",
     "C5/csr-relabel", "C5/csr5-w32s16", "C5/csr", "C5/hyb", "C5/sell-c32s8192",
-    "C4/csr5-w32s16-relabel", "C4/csr5-w32s8-relabel", "C4/sell-c32s8192-relabel", "C4/hyb-relabel",
+    "C4/csr5-w32s16-relabel", "C4/csr5-w32s8-relabel", "C4/sell-c32s0-relabel", "C4/sell-c32s8192-relabel", "C4/hyb-relabel",
     "C4/csr-relabel", "C4/csr5-w32s16", "C4/csr", "C4/hyb",
     "C3/ell", "C3/hyb", "C3/sell-c32s1024", "C3/csr5-w32s16",
     "C2/ell", "C2/hyb", "C2/csr5-w32s16",

@@ -38,7 +38,8 @@ def test_too_few_gpus_is_a_clear_error():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
-def test_two_rank_bench_code_path_over_gloo():
+@pytest.mark.parametrize("formats", ["csr5,hyb", "sell"])
+def test_two_rank_bench_code_path_over_gloo(formats):
     """bench.py --gpus 2 end to end (torchrun re-exec, row blocks, relabelled
     shards, overlapped all-gatherv, sparse exchange, e2e, max-over-ranks
     timing) with two ranks sharing this box's GPU over gloo: a check of the
@@ -48,11 +49,11 @@ def test_two_rank_bench_code_path_over_gloo():
 
     r = _run(["--gpus", "2", "--dist-backend", "gloo", "--workload", "C4", "--steps", "3", "--warmup", "3",
               "--no-configs", "--no-cpu-baseline", "--kernel-reps", "3", "--clock-ramp-s", "0.05", "--e2e-steps", "2",
-              "--formats", "csr5,hyb"])
+              "--formats", formats])
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "rowblock2"
-    assert line["config"]["format"] in ("csr5", "hyb")
-    assert line["exchange"]["overlap_ranges"] > 1 or line["config"]["format"] != "csr5"
+    assert line["config"]["format"] in formats.split(",")
+    assert line["exchange"]["overlap_ranges"] > 1 or line["config"]["format"] not in ("csr5", "sell")
     assert "ms_per_step_allgatherv" in line["exchange"] and "ms_per_step_sparse" in line["exchange"]
     assert line["gpu_launches"] > 0 and line["value"] > 0

@@ -57,13 +57,20 @@ def _worker(rank, world, port_no, steps, out, exchange, tag, n_ranges):
     bounds = spdist.nnz_balanced_bounds(csr.ptr, world)
     lo, hi = int(bounds[rank]), int(bounds[rank + 1])
     shard = spdist.row_block(csr, lo, hi)
-    m = sp.convert(tag, shard, **(dict(omega=32, sigma=16) if tag == "csr5" else {}))
+    kw = {"csr5": dict(omega=32, sigma=16), "sell": dict(sell_c=32, sell_sigma=64)}.get(tag, {})
+    m = sp.convert(tag, shard, **kw)
 
     def local_spmv(x, out_view, scale):
         sp.spmv(tag, m, x, out=out_view, scale=scale)
 
     ranges, range_fn = None, None
-    if n_ranges:
+    if n_ranges and tag == "sell":
+        splan = m.range_plan(n_ranges)[::-1]
+        ranges = [(r_[6], r_[7]) for r_ in splan]
+
+        def range_fn(k, x, out_view, scale):
+            sp.spmv_sell_range(m, x, out_view, splan[k], scale=scale)
+    elif n_ranges:
         tb, rb = m.range_plan(n_ranges)
         k_all = len(tb) - 1
         plan = [(int(rb[k]), int(rb[k + 1]) if k + 1 < k_all else m.n_rows, int(tb[k]), int(tb[k + 1]))
@@ -123,6 +130,7 @@ STEPS = 10
     (3, "allgatherv", "csr5", 3),
     (2, "sparse", "csr5", 0),
     (2, "allgatherv", "hyb", 0),
+    (2, "allgatherv", "sell", 3),
 ])
 def test_gloo_ranks_real_kernels_match_serial(cuda, world, exchange, tag, n_ranges):
     got = _run(world, STEPS, exchange, tag, n_ranges)

@@ -198,3 +198,28 @@ def test_relabelled_sell_empty_tail(sp, c, sigma):
     if int(so.widths.max()) <= 256:
         assert np_(y).tobytes() == want.tobytes()
     assert np.all(np_(y)[order.n_nonempty:] == 0.0)
+
+
+@pytest.mark.parametrize("c,sigma,k", [(32, 256, 4), (32, 0, 5), (4, 8, 3), (8, 64, 7)])
+def test_sell_ranges_bit_identical(sp, c, sigma, k):
+    """spmv_sell_range over every range of a plan (any order) == one SELL
+    SpMV, bit for bit; each range's rows are a contiguous block (ranges are
+    aligned to the sigma windows).  Degree-ordered and reference layouts."""
+    row, col, val, n = rmat_host(13, 8, 19)
+    a = sp.canonicalize(row, col, val, n, n)
+    for mat in (a, sp.DegreeOrder(a).matrix(a)):
+        m = sp.to_sell(mat, c, sigma)
+        x = torch.from_numpy(synth_ref.uniform(n, 3)).cuda()
+        s = torch.full((1,), 0.5, dtype=torch.float64, device="cuda")
+        want = sp.spmv("sell", m, x, scale=s)
+        plan = m.range_plan(k)
+        assert plan[0][6] == 0 and plan[-1][7] == n
+        assert all(plan[i][7] == plan[i + 1][6] for i in range(len(plan) - 1))
+        y = torch.full((n,), 7.0, dtype=torch.float64, device="cuda")
+        for r in plan[::-1]:
+            sp.spmv_sell_range(m, x, y, r, scale=s)
+        assert torch.equal(y, want)
+        if sigma:
+            perm = np_(m.perm)
+            for r in plan:  # a range's permuted rows are its own rows
+                assert sorted(perm[r[6]:r[7]].tolist()) == list(range(r[6], r[7]))
