@@ -17,7 +17,12 @@ canonicalizes with oracle/port.py) and the GPU result is compared there:
   (formats.py:196-250) run on it; tile_ptr, bit_flag, y_off, seg_off,
   indices and data of the GPU conversion are bit-exact against it.  y_off
   and seg_off are not read by the SpMV kernel, so only this check covers
-  them at C5 scale.
+  them at C5 scale;
+* the headline power-iteration path itself: the degree-ordered shadow layout
+  in the format bench.py times (SELL-32 sigma 0 with the 4096-column
+  wide-slice threshold and the empty-tail path; CSR5 omega 32 sigma 8),
+  mapped back through the permutation, y at the sampled rows within the
+  same tolerance.
 """
 
 from __future__ import annotations
@@ -217,3 +222,27 @@ def test_c5_hyb_rows(c5, host):
     assert np.array_equal(tr, np.repeat(rows, tc))
     assert np.array_equal(tcol, ind[~keep])
     assert tval.tobytes() == dat[~keep].tobytes()
+
+
+@pytest.mark.parametrize("tag,kw", [
+    ("sell", dict(sell_c=32, sell_sigma=0, max_cells=1 << 34)),  # the headline power-iteration format
+    ("csr5", dict(omega=32, sigma=8)),
+])
+def test_c5_shadow_layout_spmv_sampled_rows(c5, y_ref, tag, kw):
+    """The power-iteration path itself: the degree-ordered shadow layout
+    (DegreeOrder, P A P^T, x' = P x) in the format bench.py times (SELL-32
+    with the large wide-slice threshold and the empty-tail fast path), mapped
+    back with P^T: y at the sampled rows within tolerance of the oracle."""
+    sp = c5["sp"]
+    rows, ref, bound = y_ref
+    order = sp.DegreeOrder(c5["m"])
+    rm = sp.convert(tag, order.matrix(c5["m"]), **kw)
+    if tag == "sell":
+        _, n_wide, _, _, _, wide_cols, tail_from = rm.wide_plan()
+        assert wide_cols == 4096 and n_wide > 0 and tail_from == -(-order.n_nonempty // 32) * 32
+    y = order.to_old(sp.spmv(tag, rm, order.to_new(c5["x"])))
+    got = h(y[torch.from_numpy(rows).cuda()])
+    err = np.abs(got - ref)
+    assert np.all(err <= TOL * bound), (tag, float(np.max(err / np.maximum(bound, 1e-300))))
+    del rm, y, order
+    torch.cuda.empty_cache()
