@@ -35,7 +35,10 @@ __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict_
 // next four slots prefetched (rows of 8 slots or more); 3: prefetched and
 // through L1 (c < 8, rows of 8 slots or more).
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? (SPMVB_SELL_PF > 4 ? 4 : 5) : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
+#ifndef SPMVB_SELL_MINB2
+#define SPMVB_SELL_MINB2 5  // resident blocks of the prefetching (MODE 2/3) loop
+#endif
+__global__ void __launch_bounds__(256, MODE == 0 ? 8 : (MODE >= 2 ? (SPMVB_SELL_PF > 4 ? 4 : SPMVB_SELL_MINB2) : 4)) k_spmv_sell(int64_t n_rows, int64_t c, const int64_t* __restrict__ widths,
                             const int64_t* __restrict__ slice_off, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ idx, const double* __restrict__ val,
                             const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p,
