@@ -68,7 +68,7 @@ from .harness import (  # noqa: E402
     write_records,
 )
 from .kernels import (  # noqa: E402
-    BoundCall, SpmvOperator, bind, spmv, spmv_csr, spmv_csr5, spmv_csr5_push, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_many, spmv_sell,
+    BoundCall, SpmvOperator, bind, bind_range, spmv, spmv_csr, spmv_csr5, spmv_csr5_push, spmv_csr5_tiles, spmv_ell, spmv_hyb, spmv_many, spmv_sell,
     spmv_sell_range,
 )
 from .relabel import DegreeOrder, RelabelledMatrix, power_iteration  # noqa: E402

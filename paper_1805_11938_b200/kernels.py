@@ -25,7 +25,7 @@ from . import _lib
 from ._lib import LIB, check, ptr
 from .formats import Csr5Matrix, CsrMatrix, EllMatrix, FormatMatrix, FormatTag, HybMatrix, SellMatrix
 
-__all__ = ["BoundCall", "SpmvOperator", "bind", "plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push",
+__all__ = ["BoundCall", "SpmvOperator", "bind", "bind_range", "plan_row_blocks", "spmv", "spmv_csr", "spmv_csr5", "spmv_csr5_push",
            "spmv_csr5_tiles", "spmv_ell", "spmv_hyb", "spmv_many", "spmv_sell", "spmv_sell_range"]
 
 
@@ -399,6 +399,38 @@ def bind(tag: FormatTag, m: FormatMatrix, x: torch.Tensor, out: torch.Tensor, sc
     scratch = scratch_fn(m)
     name, args = args_fn(m, x, out, ptr(scale) if scale is not None else None, scratch)
     return BoundCall(name, args, _lib.stream(m.device), keep=(m, x, out, scale, scratch))
+
+
+def bind_range(tag: FormatTag, m: FormatMatrix, x: torch.Tensor, out: torch.Tensor, r, scale=None,
+               carry: torch.Tensor | None = None) -> BoundCall:
+    """A prepared row range of a CSR5 or SELL SpMV (``spmv_csr5_tiles`` /
+    ``spmv_sell_range``): ``r`` is (row_begin, row_end, t_begin, t_end) for
+    CSR5 (from ``m.range_plan``) or an entry of ``SellMatrix.range_plan``.
+    ``out`` is the whole output vector of ``m`` (n_rows)."""
+    tag = FormatTag(tag)
+    for t, n, what in ((x, m.n_cols, "x"), (out, m.n_rows, "out")):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                and t.numel() == n and t.device == m.device):
+            raise ValueError(f"{what} must be a contiguous float64 CUDA tensor of {n} elements on {m.device}")
+    sp = ptr(scale) if scale is not None else None
+    st = _lib.stream(m.device)
+    if tag is FormatTag.CSR5 and isinstance(m, Csr5Matrix):
+        a, b, t0, t1 = (int(v) for v in r)
+        if carry is None:
+            carry = torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
+        args = (m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.tile_ptr), ptr(m.bit_flag),
+                ptr(_packed_flags(m)), ptr(m.indices), ptr(m.data), ptr(m.tile_aux), ptr(m.nonempty_rows),
+                m.n_nonempty, ptr(carry), ptr(x), ptr(out), sp, t0, t1, a, b)
+        return BoundCall("spmvb_spmv_csr5_tiles", args, st, keep=(m, x, out, scale, carry))
+    if tag is FormatTag.SELL and isinstance(m, SellMatrix):
+        wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from = m.wide_plan()
+        perm = m.perm if m.sigma > 0 else None
+        s0, s1, i0, i1, pc0, pc1 = (int(v) for v in r[:6])
+        args = (m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
+                ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, tail_from, max_narrow, ptr(x), ptr(out), sp,
+                s0, s1, i0, i1, pc0, pc1)
+        return BoundCall("spmvb_spmv_sell_range", args, st, keep=(m, x, out, scale))
+    raise ValueError(f"row ranges exist for csr5 and sell matrices, not {tag.value!r} / {type(m).__name__}")
 
 
 class SpmvOperator:

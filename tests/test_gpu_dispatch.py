@@ -112,3 +112,28 @@ def test_fast_power_iteration(sp, tag, kw):
         scale = 1.0 / np.sqrt(np.dot(y, y))
         x = y
     np.testing.assert_allclose(fast.x.cpu().numpy(), x, rtol=1e-9, atol=1e-12 * np.abs(x).max())
+
+
+@pytest.mark.parametrize("tag,kw", [("csr5", dict(omega=32, sigma=16)), ("csr5", dict(omega=32, sigma=8)),
+                                    ("sell", dict(sell_c=32, sell_sigma=0)), ("sell", dict(sell_c=8, sell_sigma=64))])
+def test_bind_range_bit_identical(sp, tag, kw):
+    """Prepared row ranges (bind_range, used by the multi-GPU overlap) over a
+    range plan == one SpMV, bit for bit."""
+    a = _matrix(sp, "rmat")
+    m = sp.convert(tag, a, **kw)
+    x = sp.synth.uniform_vector(a.n_cols, 9)
+    s = torch.full((1,), 1.5, dtype=torch.float64, device="cuda")
+    want = sp.spmv(tag, m, x, scale=s)
+    if tag == "csr5":
+        tb, rb = m.range_plan(4)
+        k = len(tb) - 1
+        plan = [(int(rb[i]), int(rb[i + 1]) if i + 1 < k else m.n_rows, int(tb[i]), int(tb[i + 1])) for i in range(k)]
+    else:
+        plan = m.range_plan(4)
+    y = torch.full((a.n_rows,), 3.0, dtype=torch.float64, device="cuda")
+    calls = [sp.bind_range(tag, m, x, y, r, s) for r in plan[::-1]]
+    for c in calls:
+        c()
+    assert torch.equal(y, want)
+    with pytest.raises(ValueError, match="row ranges"):
+        sp.bind_range("hyb", sp.to_hyb(a), x, y, plan[0])
