@@ -705,13 +705,31 @@ def run_ours(args):
             sp.spmv_csr5_push(m, xv, out, peers, off, scale=scale, carry=carry_p)
 
     def make_pi(exchange):
+        if exchange == "allgatherv" and world > 1 and args.dist_backend == "nccl" and args.driver == "native":
+            # the C ABI's step (spmvb_dist_*): NCCL issued from C, one ctypes
+            # call per step; the torch.distributed driver issues every P2P op
+            # from Python, tens of microseconds each (14 per range at N = 8)
+            comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
+            return spdist.NativePowerIteration(
+                local_spmv, bounds, rank, world, dev, x_run, comm, ranges=ranges,
+                range_op=(lambda k, xv, out, sc: sp.bind_range(tag, m, xv, out, rplan[k], sc, carry=carry))
+                if ranges else None)
+        if exchange == "allgatherv-torch":
+            exchange = "allgatherv"
         return spdist.PowerIteration(local_spmv, bounds, rank, world, dev, x_run, exchange=exchange,
                                      local_cols=shard_run.indices if exchange == "sparse" else None,
                                      local_ranges=ranges if exchange in ("allgatherv", "p2p") else None,
                                      local_spmv_range=range_fn,
                                      local_spmv_push=push_fn if exchange == "p2p" else None)
 
-    pi = make_pi(args.exchange)
+    native_error = None
+    try:
+        pi = make_pi(args.exchange)
+    except Exception as exc:  # e.g. no NCCL communicator pointer in this torch: the torch driver instead
+        if args.exchange != "allgatherv" or world == 1:
+            raise
+        native_error = f"{type(exc).__name__}: {str(exc)[:160]}"
+        pi = make_pi("allgatherv-torch")
     for _ in range(warmup):
         pi.step()
     torch.cuda.synchronize()
@@ -761,15 +779,20 @@ def run_ours(args):
         t_loop = float(tt.item())
     value = 2.0 * nnz * args.steps / t_loop / 1e9
     eig = pi.eigenvalue_estimate()
-    exchange = {"mode": pi.exchange, "overlap_ranges": len(ranges) if ranges else 1,
+    exchange = {"mode": pi.exchange, "driver": getattr(pi, "driver", "torch.distributed (dist.PowerIteration)"),
+                "native_driver_error": native_error,
+                "overlap_ranges": len(ranges) if ranges else 1,
                 f"ms_per_step_{pi.exchange}": t_loop / args.steps * 1e3}
     if world > 1:
         # the other exchanges, same steps, for comparison (report
         # the all-gather and the sparse exchange; p2p = our kernels over NVLink)
         vol = getattr(pi, "exchange_volume", None)
         mode = pi.exchange
+        native = hasattr(pi, "driver")
         del pi
-        others = ("allgatherv", "sparse", "p2p") if args.compare_p2p else ("allgatherv", "sparse")
+        others = ["allgatherv", "sparse"] + (["p2p"] if args.compare_p2p else [])
+        if native:  # the C-ABI driver ran the headline: time the torch one beside it
+            others[0] = "allgatherv-torch"
         for other in others:
             if other == mode:
                 continue
@@ -970,6 +993,8 @@ def main():
                     help="p2p exchange with a separate push kernel per row range instead of the fused SpMV+push")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: ranks may share GPUs (checks the N > 1 code path on a small box; not a measurement)")
+    ap.add_argument("--driver", choices=["native", "torch"], default="native",
+                    help="N > 1 all-gatherv: the C ABI's spmvb_dist_* step (default) or the torch.distributed driver")
     ap.add_argument("--clock-ramp-s", type=float, default=1.0)
     ap.add_argument("--cpu-sample", choices=["auto", "full", "rows"], default="auto",
                     help="CPU reference on R-MAT: the whole matrix (auto: when the host RAM allows) or a row sample")

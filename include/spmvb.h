@@ -356,6 +356,23 @@ int spmvb_dist_init(void* nccl_comm, int rank, int world, const int64_t* bounds,
 int spmvb_dist_step(spmvb_dist* d, spmvb_local_spmv_fn local_spmv, void* ctx, const double* x, double* x_next,
                     double* sumsq, double* scale, void* stream);
 int spmvb_dist_destroy(spmvb_dist* d);
+/* The version (NCCL_VERSION_CODE) of the libnccl.so.2 the dist entry points
+ * resolved: it must be the one that created the caller's communicator. */
+int spmvb_dist_nccl_version(int* version);
+/* The same step with the exchange overlapped: the shard is computed as
+ * n_ranges row ranges (spans: world * n_ranges * 2 local row bounds [a, b)
+ * of every rank's ranges, the same array on every rank; empty = a == b), and
+ * each range's rows are sent to the peers on an internal exchange stream
+ * while the next range computes.  range_spmv(ctx, k, x, y_local, scale,
+ * stream) computes this rank's range k into y_local (the shard's rows).
+ * Range bounds must not split a row's computation (e.g. CSR5 range_plan,
+ * SELL range_plan); then x_next is the same, bit for bit, as spmvb_dist_step. */
+typedef int (*spmvb_range_spmv_fn)(void* ctx, int k, const double* x, double* y_local, const double* scale,
+                                   void* stream);
+int spmvb_dist_init_ranges(void* nccl_comm, int rank, int world, const int64_t* bounds, int n_ranges,
+                           const int64_t* spans, spmvb_dist** out);
+int spmvb_dist_step_ranges(spmvb_dist* d, spmvb_range_spmv_fn range_spmv, void* ctx, const double* x,
+                           double* x_next, double* sumsq, double* scale, void* stream);
 
 /* Degree-ordered symmetric relabelling (relabel.cu): an internal shadow
  * layout P A P^T of a square n x n CSR for iterative SpMV (power iteration

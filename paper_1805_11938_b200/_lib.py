@@ -118,6 +118,9 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_dist_init": (c_int, [vp, c_int, c_int, vp, P_vp]),
     "spmvb_dist_step": (c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_dist_destroy": (c_int, [vp]),
+    "spmvb_dist_nccl_version": (c_int, [ctypes.POINTER(c_int)]),
+    "spmvb_dist_init_ranges": (c_int, [vp, c_int, c_int, vp, c_int, vp, P_vp]),
+    "spmvb_dist_step_ranges": (c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_sum_inv_sqrt": (c_int, [vp, c_int, vp, vp, vp]),
     "spmvb_gather_probe_threads": (c_i64, []),
     "spmvb_gather_probe": (c_int, [vp, vp, c_i64, vp, vp]),

@@ -26,6 +26,14 @@ struct spmvb_dist {
   ncclComm_t comm;
   int rank, world;
   std::vector<int64_t> bounds;
+  int n_ranges = 0;             // K: row ranges per step (0: the whole shard at once)
+  std::vector<int64_t> spans;   // world * K * 2: rank p's range k = local rows [a, b)
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> events;
+  ~spmvb_dist() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+  }
 };
 
 namespace {
@@ -37,6 +45,7 @@ struct Nccl {
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclGetVersion) get_version = nullptr;
   bool ok = false;
 };
 
@@ -53,7 +62,8 @@ const Nccl& nccl() {
     n.group_start = reinterpret_cast<decltype(&ncclGroupStart)>(dlsym(h, "ncclGroupStart"));
     n.group_end = reinterpret_cast<decltype(&ncclGroupEnd)>(dlsym(h, "ncclGroupEnd"));
     n.error_string = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    n.ok = n.all_reduce && n.send && n.recv && n.group_start && n.group_end && n.error_string;
+    n.get_version = reinterpret_cast<decltype(&ncclGetVersion)>(dlsym(h, "ncclGetVersion"));
+    n.ok = n.all_reduce && n.send && n.recv && n.group_start && n.group_end && n.error_string && n.get_version;
   });
   if (!n.ok) fail(SPMVB_INTERNAL, "libnccl.so.2 could not be loaded (needed by the spmvb_dist_* entry points)");
   return n;
@@ -71,6 +81,13 @@ void forward(int st) {  // a nested C-ABI call's failure, message kept
 }
 
 }  // namespace
+
+extern "C" int spmvb_dist_nccl_version(int* version) {
+  return guard([&] {
+    if (!version) fail(SPMVB_INVALID_ARG, "version is required");
+    nccl_check(nccl().get_version(version), "ncclGetVersion");
+  });
+}
 
 extern "C" int spmvb_dist_init(void* nccl_comm, int rank, int world, const int64_t* bounds, spmvb_dist** out) {
   return guard([&] {
@@ -109,6 +126,82 @@ extern "C" int spmvb_dist_step(spmvb_dist* d, spmvb_local_spmv_fn local_spmv, vo
         if (phi > plo) nccl_check(n.recv(x_next + plo, phi - plo, ncclFloat64, p, d->comm, s), "ncclRecv");
       }
       nccl_check(n.group_end(), "ncclGroupEnd");
+    }
+    forward(spmvb_inv_sqrt(sumsq, scale, stream));
+  });
+}
+
+extern "C" int spmvb_dist_init_ranges(void* nccl_comm, int rank, int world, const int64_t* bounds, int n_ranges,
+                                      const int64_t* spans, spmvb_dist** out) {
+  return guard([&] {
+    if (const int st = spmvb_dist_init(nccl_comm, rank, world, bounds, out)) forward(st);
+    spmvb_dist* d = *out;
+    *out = nullptr;
+    auto fail_free = [&](const char* msg) {
+      delete d;
+      fail(SPMVB_INVALID_ARG, "%s", msg);
+    };
+    if (n_ranges < 1 || !spans) fail_free("n_ranges >= 1 and spans (world * n_ranges * 2) are required");
+    for (int p = 0; p < world; ++p)
+      for (int k = 0; k < n_ranges; ++k) {
+        const int64_t a = spans[(p * n_ranges + k) * 2], b = spans[(p * n_ranges + k) * 2 + 1];
+        if (a < 0 || b < a || b > bounds[p + 1] - bounds[p]) fail_free("a range lies outside its rank's rows");
+      }
+    d->n_ranges = n_ranges;
+    d->spans.assign(spans, spans + static_cast<size_t>(world) * n_ranges * 2);
+    if (cudaStreamCreateWithFlags(&d->comm_stream, cudaStreamNonBlocking) != cudaSuccess)
+      fail_free("could not create the exchange stream");
+    d->events.resize(n_ranges + 2, nullptr);
+    for (auto& e : d->events)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) fail_free("could not create events");
+    *out = d;
+  });
+}
+
+// Ranges in order k = 0..K-1 on the caller's stream; after each one its rows
+// go to every peer (and the peers' range-k rows come in) on the exchange
+// stream while range k+1 computes.  Every rank walks the same k, so the k-th
+// NCCL groups pair up.  Then ||y||^2 (all-reduce on the exchange stream, in
+// the same order on every rank), and the caller's stream waits for the
+// exchange before 1/||y||.
+extern "C" int spmvb_dist_step_ranges(spmvb_dist* d, spmvb_range_spmv_fn range_spmv, void* ctx, const double* x,
+                                      double* x_next, double* sumsq, double* scale, void* stream) {
+  return guard([&] {
+    if (!d || !range_spmv) fail(SPMVB_INVALID_ARG, "handle and range SpMV are required");
+    if (d->n_ranges < 1) fail(SPMVB_INVALID_ARG, "the handle has no range plan (spmvb_dist_init_ranges)");
+    if (!x || !x_next || !sumsq || !scale) fail(SPMVB_INVALID_ARG, "x, x_next, sumsq and scale are required");
+    cudaStream_t s = as_stream(stream), cs = d->comm_stream;
+    const int K = d->n_ranges, me = d->rank;
+    const int64_t lo = d->bounds[me], hi = d->bounds[me + 1];
+    auto span = [&](int p, int k, int64_t& a, int64_t& b) {
+      a = d->spans[(static_cast<size_t>(p) * K + k) * 2];
+      b = d->spans[(static_cast<size_t>(p) * K + k) * 2 + 1];
+    };
+    const Nccl& n = nccl();
+    for (int k = 0; k < K; ++k) {
+      int64_t a, b;
+      span(me, k, a, b);
+      if (b > a) forward(range_spmv(ctx, k, x, x_next + lo, scale, stream));
+      if (d->world == 1) continue;
+      SPMVB_CUDA(cudaEventRecord(d->events[k], s));
+      SPMVB_CUDA(cudaStreamWaitEvent(cs, d->events[k], 0));
+      nccl_check(n.group_start(), "ncclGroupStart");
+      for (int p = 0; p < d->world; ++p) {
+        if (p == me) continue;
+        int64_t pa, pb;
+        span(p, k, pa, pb);
+        if (b > a) nccl_check(n.send(x_next + lo + a, b - a, ncclFloat64, p, d->comm, cs), "ncclSend");
+        if (pb > pa) nccl_check(n.recv(x_next + d->bounds[p] + pa, pb - pa, ncclFloat64, p, d->comm, cs), "ncclRecv");
+      }
+      nccl_check(n.group_end(), "ncclGroupEnd");
+    }
+    forward(spmvb_sumsq(x_next + lo, hi - lo, sumsq, stream));
+    if (d->world > 1) {
+      SPMVB_CUDA(cudaEventRecord(d->events[K], s));
+      SPMVB_CUDA(cudaStreamWaitEvent(cs, d->events[K], 0));
+      nccl_check(n.all_reduce(sumsq, sumsq, 1, ncclFloat64, ncclSum, d->comm, cs), "ncclAllReduce");
+      SPMVB_CUDA(cudaEventRecord(d->events[K + 1], cs));
+      SPMVB_CUDA(cudaStreamWaitEvent(s, d->events[K + 1], 0));
     }
     forward(spmvb_inv_sqrt(sumsq, scale, stream));
   });

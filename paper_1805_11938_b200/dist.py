@@ -628,18 +628,25 @@ class PowerIteration:
 
 class NativePowerIteration:
     """The row-block power iteration through the C ABI's ``spmvb_dist_*``
-    (a caller-owned NCCL communicator), for parity with what a
-    non-Python caller gets.  ``local_op`` binds the shard's SpMV
-    (``kernels.SpmvOperator`` or ``relabel.RelabelledMatrix``);
+    (a caller-owned NCCL communicator): one ctypes call per
+    step, NCCL issued from C, no per-op Python work.  ``local_op`` binds the
+    shard's SpMV (``kernels.SpmvOperator`` or ``relabel.RelabelledMatrix``);
     ``comm_ptr`` is the ``ncclComm_t`` address (from torch:
-    ``group._get_backend(device)._comm_ptr()``).  Same step as
-    ``PowerIteration``'s all-gatherv path, bit for bit."""
+    ``group._get_backend(device)._comm_ptr()``).  With ``ranges`` (this
+    rank's local row spans in execution order) and ``range_op(k, x, out,
+    scale)`` returning a prepared launch of span k (``kernels.bind_range``), each
+    span's rows go to the peers while the next span computes
+    (``spmvb_dist_step_ranges``); the spans of all ranks are exchanged once
+    here over ``group``.  Same iterate as ``PowerIteration``'s all-gatherv
+    path, bit for bit."""
 
     _CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p)
+    _RCB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_void_p, ctypes.c_void_p)
 
     def __init__(self, local_op, bounds, rank: int, world: int, device: torch.device, x0: torch.Tensor,
-                 comm_ptr: int):
+                 comm_ptr: int, ranges=None, range_op: Callable | None = None, group=None):
         self.bounds = [int(b) for b in bounds]
         self.rank, self.world, self.device = rank, world, device
         n = self.bounds[-1]
@@ -648,28 +655,67 @@ class NativePowerIteration:
         self.x_next = torch.empty(n, dtype=torch.float64, device=device)
         self.sumsq = torch.zeros(1, dtype=torch.float64, device=device)
         self.scale = torch.ones(1, dtype=torch.float64, device=device)
-        # the SpMV of each parity, bound once; the callback picks it by x
-        self._calls = {int(a.data_ptr()): local_op.bind(a, b[lo:hi], self.scale)
-                       for a, b in ((self.x, self.x_next), (self.x_next, self.x))}
+        pairs = ((self.x, self.x_next), (self.x_next, self.x))
+        self._ranged = ranges is not None
+        if self._ranged:
+            if range_op is None:
+                raise ValueError("ranges need range_op")
+            spans = [(int(a), int(b)) for a, b in ranges]
+            allspans = [None] * world
+            if world > 1:
+                dist.all_gather_object(allspans, spans, group=group)
+            else:
+                allspans = [spans]
+            K = max(len(sp_) for sp_ in allspans)
+            flat = []
+            for sp_ in allspans:
+                sp_ = sp_ + [(0, 0)] * (K - len(sp_))
+                flat += [v for ab in sp_ for v in ab]
+            self._calls = {(int(a.data_ptr()), k): range_op(k, a, b[lo:hi], self.scale) for a, b in pairs
+                           for k in range(len(spans))}
 
-        def local(ctx, x, y, scale, stream):
-            try:
-                self._calls[int(x)]()
-                return 0
-            except Exception:  # reported through the status code
-                return _lib.SPMVB_INTERNAL
+            def local(ctx, k, x, y, scale, stream):
+                try:
+                    self._calls[(int(x), int(k))]()
+                    return 0
+                except Exception:  # reported through the status code
+                    return _lib.SPMVB_INTERNAL
 
-        self._cb = self._CB(local)  # keep the callback alive with the object
-        b = (ctypes.c_int64 * len(self.bounds))(*self.bounds)
-        h = ctypes.c_void_p()
-        check(LIB.spmvb_dist_init(ctypes.c_void_p(comm_ptr), rank, world, b, ctypes.byref(h)))
+            self._cb = self._RCB(local)
+            b_arr = (ctypes.c_int64 * len(self.bounds))(*self.bounds)
+            s_arr = (ctypes.c_int64 * len(flat))(*flat)
+            h = ctypes.c_void_p()
+            check(LIB.spmvb_dist_init_ranges(ctypes.c_void_p(comm_ptr), rank, world, b_arr, K, s_arr,
+                                             ctypes.byref(h)))
+        else:
+            # the SpMV of each parity, bound once; the callback picks it by x
+            self._calls = {int(a.data_ptr()): local_op.bind(a, b[lo:hi], self.scale) for a, b in pairs}
+
+            def local(ctx, x, y, scale, stream):
+                try:
+                    self._calls[int(x)]()
+                    return 0
+                except Exception:  # reported through the status code
+                    return _lib.SPMVB_INTERNAL
+
+            self._cb = self._CB(local)  # keep the callback alive with the object
+            b_arr = (ctypes.c_int64 * len(self.bounds))(*self.bounds)
+            h = ctypes.c_void_p()
+            check(LIB.spmvb_dist_init(ctypes.c_void_p(comm_ptr), rank, world, b_arr, ctypes.byref(h)))
         self._h = h
+        self.exchange = "allgatherv"
+        self.driver = "c-abi spmvb_dist_step" + ("_ranges" if self._ranged else "")
 
     def step(self) -> None:
+        fn = LIB.spmvb_dist_step_ranges if self._ranged else LIB.spmvb_dist_step
         with torch.cuda.device(self.device):
-            check(LIB.spmvb_dist_step(self._h, ctypes.cast(self._cb, ctypes.c_void_p), None, ptr(self.x),
-                                      ptr(self.x_next), ptr(self.sumsq), ptr(self.scale), _lib.stream(self.device)))
+            check(fn(self._h, ctypes.cast(self._cb, ctypes.c_void_p), None, ptr(self.x), ptr(self.x_next),
+                     ptr(self.sumsq), ptr(self.scale), _lib.stream(self.device)))
         self.x, self.x_next = self.x_next, self.x
+
+    def eigenvalue_estimate(self) -> float:
+        s = float(self.scale.item())
+        return 1.0 / s if s > 0 else math.nan
 
     def close(self) -> None:
         if getattr(self, "_h", None):
