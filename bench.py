@@ -563,10 +563,14 @@ def run_ours(args):
     if relabel:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        order = DegreeOrder(csr_full)
+        # N > 1: the degree-sorted rows dealt round-robin to the ranks' blocks
+        # (DegreeOrder(parts=N)): nnz-balanced to within one row, and every
+        # block holds the same mix of hub and light rows (profiles/
+        # r02_shard_balance.txt: compute-side efficiency at 8 shards 0.94 vs
+        # 0.81 for nnz-balanced cuts of one degree order)
+        order = DegreeOrder(csr_full, parts=world)
         csr_run = order.matrix(csr_full)
-        bounds = (spdist.cost_balanced_bounds(csr_run.ptr, world) if args.balance == "cost"
-                  else spdist.nnz_balanced_bounds(csr_run.ptr, world))
+        bounds = order.part_bounds if world > 1 else [0, csr_run.n_rows]
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         shard_run = spdist.row_block(csr_run, lo, hi) if world > 1 else csr_run
         x_run = order.to_new(x_full)
@@ -899,7 +903,8 @@ def run_ours(args):
             "config": {"workload": args.workload, "desc": w["desc"], "format": tag, "variant": label,
                        "params": {k: v for k, v in kw.items() if k != "max_cells"}, "n": n,
                        "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
-                       "balance": args.balance,
+                       "balance": ("degree-sorted rows dealt round-robin to the rank blocks (nnz-balanced to "
+                                   "within one row)" if relabel and world > 1 else args.balance),
                        "layout": ("degree-ordered shadow P A P^T (relabel.py), iterate x' = P x; the reference-layout "
                                   "matrix serves the e2e calls" if relabel else "reference layout"),
                        "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"

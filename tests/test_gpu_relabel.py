@@ -223,3 +223,39 @@ def test_sell_ranges_bit_identical(sp, c, sigma, k):
             perm = np_(m.perm)
             for r in plan:  # a range's permuted rows are its own rows
                 assert sorted(perm[r[6]:r[7]].tolist()) == list(range(r[6], r[7]))
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_dealt_order_blocks(sp, parts):
+    """DegreeOrder(parts=P) (the multi-GPU form): the degree-sorted ids dealt
+    round-robin to P contiguous blocks; each block is in sorted order with
+    its empty rows last, blocks are nnz-balanced to within one row, and the
+    SpMV of the dealt matrix maps back to A x within tolerance."""
+    row, col, val, n = rmat_host(12, 8, 23)
+    a = sp.canonicalize(row, col, val, n, n)
+    csr = sp.to_csr(a)
+    one = sp.DegreeOrder(csr)
+    dealt = sp.DegreeOrder(csr, parts=parts)
+    sorted_old = np_(one.perm)  # old ids in degree order
+    b = dealt.part_bounds
+    assert b[0] == 0 and b[-1] == n and len(b) == parts + 1
+    perm = np_(dealt.perm)
+    for p in range(parts):
+        assert perm[b[p]:b[p + 1]].tolist() == sorted_old[p::parts].tolist()
+    new_id = np_(dealt.new_id)
+    assert np.array_equal(new_id[perm], np.arange(n))
+    m = dealt.matrix(csr)
+    rowdeg = np.diff(np_(m.ptr))
+    nnz = [int(rowdeg[b[p]:b[p + 1]].sum()) for p in range(parts)]
+    assert max(nnz) - min(nnz) <= int(rowdeg.max())
+    for p in range(parts):  # empty rows last within each block
+        d = rowdeg[b[p]:b[p + 1]]
+        k = int((d > 0).sum())
+        assert np.all(d[:k] > 0) and np.all(d[k:] == 0)
+    x = synth_ref.uniform(n, 5)
+    ref = port.dense_spmv_oracle(row, col, val, n, x)
+    bound = port.dense_spmv_oracle(row, col, np.abs(val), n, np.abs(x))
+    xd = torch.from_numpy(x).cuda()
+    for tag, kw in [("csr5", dict(omega=32, sigma=8)), ("sell", dict(sell_c=32, sell_sigma=0))]:
+        y = dealt.to_old(sp.spmv(tag, sp.convert(tag, m, **kw), dealt.to_new(xd)))
+        assert np.all(np.abs(np_(y) - ref) <= TOL * bound), tag
