@@ -150,10 +150,13 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
   }
 }
 
-// Warp per (wide slice, row): lane k adds pieces k, k+32, ... in order, then
-// the xor butterfly (a fixed order: deterministic).  A thread per row adding
-// its pieces one after another was a chain of dependent loads as long as the
-// row's piece count (~400 for a degree-ordered C5 hub row: 41 us).
+// Warp per wide slice.  A slice of few pieces (<= 32: the common case in a
+// reference-layout power-law matrix) is summed a row per lane, pieces in
+// order; a slice of many (a degree-ordered matrix's hub rows, ~400 pieces at
+// C5) row by row with the whole warp -- lane k adds pieces k, k+32, ..., then
+// the xor butterfly -- instead of one lane walking ~400 dependent loads
+// (41 us).  The order depends only on the slice's piece count:
+// deterministic.
 __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
                                   const int32_t* __restrict__ first_piece, int64_t n_pieces,
                                   const double* __restrict__ part, const int32_t* __restrict__ perm,
@@ -164,19 +167,28 @@ __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __re
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t q = i_begin * c + warp; q < i_end * c; q += nwarps) {
-    const int64_t i = q / c;
-    const int l = static_cast<int>(q - i * c);
+  auto store = [&](int64_t sl, int l, double sum) {
+    const int64_t p = sl * c + l;
+    const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
+    y[r] = scale_p ? sc * sum : sum;
+  };
+  for (int64_t i = i_begin + warp; i < i_end; i += nwarps) {
     const int64_t sl = wide[i];
-    if (l >= sell_rows(sl, c, n_rows)) continue;
+    const int rows = sell_rows(sl, c, n_rows);
     const int32_t p0 = first_piece[i], p1 = i + 1 < n_wide ? first_piece[i + 1] : static_cast<int32_t>(n_pieces);
-    double sum = 0.0;
-    for (int32_t pc = p0 + lane; pc < p1; pc += 32) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
-    sum = warp_sum(sum);
-    if (lane == 0) {
-      const int64_t p = sl * c + l;
-      const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
-      y[r] = scale_p ? sc * sum : sum;
+    if (p1 - p0 <= 32) {
+      for (int l = lane; l < rows; l += 32) {
+        double sum = 0.0;
+        for (int32_t pc = p0; pc < p1; ++pc) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
+        store(sl, l, sum);
+      }
+    } else {
+      for (int l = 0; l < rows; ++l) {
+        double sum = 0.0;
+        for (int32_t pc = p0 + lane; pc < p1; pc += 32) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
+        sum = warp_sum(sum);
+        if (lane == 0) store(sl, l, sum);
+      }
     }
   }
 }
@@ -286,7 +298,7 @@ void sell_launch(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t
                n_wide, first_piece, n_pieces, widths, slice_off, idx, val, x, part.get(),
                static_cast<int32_t>(pc_begin), static_cast<int32_t>(pc_end));
     SPMVB_LAUNCHED("k_sell_wide_part");
-    launch_pdl(k_sell_wide_final, dim3(grid_for((i_end - i_begin) * c * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows,
+    launch_pdl(k_sell_wide_final, dim3(grid_for((i_end - i_begin) * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows,
                c, wide, n_wide, first_piece, n_pieces, part.get(), perm, y, scale, i_begin, i_end);
     SPMVB_LAUNCHED("k_sell_wide_final");
   }
