@@ -296,23 +296,31 @@ int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* widths, int64
 /* tail_from (n_rows = none): the caller's promise that every permuted row
  * p >= tail_from is empty with perm[p] == p (a degree-ordered matrix's empty
  * tail); those rows get y = 0 without any slice or perm lookups. */
+/* hub (device, may be NULL when n_hub == 0): the ascending indices into the
+ * wide list of the wide slices with more than SPMVB_SELL_HUB_PIECES pieces;
+ * their rows are summed a warp per row, the other wide rows a thread per
+ * row. */
+#define SPMVB_SELL_HUB_PIECES 32
 int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                     const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
-                    const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols, int64_t tail_from,
-                    int64_t max_narrow_width, const double* x, double* y, const double* scale, void* stream);
+                    const int32_t* first_piece, int64_t n_pieces, const int32_t* hub, int64_t n_hub,
+                    int64_t wide_cols, int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
+                    const double* scale, void* stream);
 /* Slices [s_begin, s_end) of spmvb_spmv_sell (e.g. to send finished rows to
  * other GPUs while later slices compute): [i_begin, i_end) = the entries of
  * the wide list whose slices lie in the range, [pc_begin, pc_end) = their
- * pieces (first_piece[i_begin] .. first_piece[i_end], or n_pieces).  Over a
+ * pieces (first_piece[i_begin] .. first_piece[i_end], or n_pieces),
+ * [h_begin, h_end) = the hub entries among them.  Over a
  * partition of the slices, the same y as one spmvb_spmv_sell, bit for bit;
  * with sigma > 0 a range's rows are perm[s_begin*c .. s_end*c), contiguous
  * when the range is aligned to sorting windows. */
 int spmvb_spmv_sell_range(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                           const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
-                          int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
-                          int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
-                          const double* scale, int64_t s_begin, int64_t s_end, int64_t i_begin, int64_t i_end,
-                          int64_t pc_begin, int64_t pc_end, void* stream);
+                          int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, const int32_t* hub,
+                          int64_t n_hub, int64_t wide_cols, int64_t tail_from, int64_t max_narrow_width,
+                          const double* x, double* y, const double* scale, int64_t s_begin, int64_t s_end,
+                          int64_t i_begin, int64_t i_end, int64_t pc_begin, int64_t pc_end, int64_t h_begin,
+                          int64_t h_end, void* stream);
 
 /* ||y||^2 over n entries into *out (device), deterministic two-level sum.
  * Used by power iteration. */

@@ -101,10 +101,10 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "spmvb_spmv_ell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp]),
     "spmvb_sell_wide_plan": (c_int, [c_i64, c_i64, vp, c_i64, vp, P_i64, P_i64, vp, P_i64, vp]),
-    "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, c_i64, c_i64, c_i64, vp, vp,
-                                vp, vp]),
-    "spmvb_spmv_sell_range": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, c_i64, c_i64, c_i64, vp,
-                                      vp, vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, vp]),
+    "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, vp, c_i64, c_i64, c_i64,
+                                c_i64, vp, vp, vp, vp]),
+    "spmvb_spmv_sell_range": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, vp, c_i64, c_i64, c_i64,
+                                      c_i64, vp, vp, vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, vp]),
     "spmvb_sumsq": (c_int, [vp, c_i64, vp, vp]),
     "spmvb_inv_sqrt": (c_int, [vp, vp, vp]),
     "spmvb_norm_ws_bytes": (c_i64, []),

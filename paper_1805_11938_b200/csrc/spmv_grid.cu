@@ -150,13 +150,13 @@ __global__ void __launch_bounds__(256) k_sell_wide_part(int64_t n_rows, int64_t 
   }
 }
 
-// Warp per wide slice.  A slice of few pieces (<= 32: the common case in a
-// reference-layout power-law matrix) is summed a row per lane, pieces in
-// order; a slice of many (a degree-ordered matrix's hub rows, ~400 pieces at
-// C5) row by row with the whole warp -- lane k adds pieces k, k+32, ..., then
-// the xor butterfly -- instead of one lane walking ~400 dependent loads
-// (41 us).  The order depends only on the slice's piece count:
-// deterministic.
+// The rows of the wide slices, summed from their pieces in a fixed order:
+// deterministic.  A slice of at most SPMVB_SELL_HUB_PIECES pieces (the
+// common case; a reference-layout power-law matrix has ~1e5 of them) is a
+// thread per row adding its pieces in order.  Slices with more pieces (a
+// degree-ordered matrix's hub rows, ~400 pieces at C5) are listed in `hub`
+// and summed by k_sell_wide_hub instead: one thread walking ~400 dependent
+// loads took 41 us.
 __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
                                   const int32_t* __restrict__ first_piece, int64_t n_pieces,
                                   const double* __restrict__ part, const int32_t* __restrict__ perm,
@@ -164,31 +164,48 @@ __global__ void k_sell_wide_final(int64_t n_rows, int64_t c, const int32_t* __re
                                   int64_t i_end) {
   pdl_wait();
   const double sc = load_scale(scale_p);
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  auto store = [&](int64_t sl, int l, double sum) {
+  for (int64_t q = i_begin * c + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < i_end * c;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = q / c;
+    const int l = static_cast<int>(q - i * c);
+    const int64_t sl = wide[i];
+    if (l >= sell_rows(sl, c, n_rows)) continue;
+    const int32_t p0 = first_piece[i], p1 = i + 1 < n_wide ? first_piece[i + 1] : static_cast<int32_t>(n_pieces);
+    if (p1 - p0 > SPMVB_SELL_HUB_PIECES) continue;  // k_sell_wide_hub's slice
+    double sum = 0.0;
+    for (int32_t pc = p0; pc < p1; ++pc) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
     const int64_t p = sl * c + l;
     const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
     y[r] = scale_p ? sc * sum : sum;
-  };
-  for (int64_t i = i_begin + warp; i < i_end; i += nwarps) {
+  }
+}
+
+// Warp per (hub slice, row): lane k adds pieces k, k+32, ... in order, then
+// the xor butterfly.  hub[h] = index into the wide list.
+__global__ void k_sell_wide_hub(int64_t n_rows, int64_t c, const int32_t* __restrict__ wide, int64_t n_wide,
+                                const int32_t* __restrict__ first_piece, int64_t n_pieces,
+                                const int32_t* __restrict__ hub, const double* __restrict__ part,
+                                const int32_t* __restrict__ perm, double* __restrict__ y,
+                                const double* __restrict__ scale_p, int64_t h_begin, int64_t h_end) {
+  pdl_wait();
+  const double sc = load_scale(scale_p);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = h_begin * c + warp; q < h_end * c; q += nwarps) {
+    const int64_t h = q / c;
+    const int l = static_cast<int>(q - h * c);
+    const int64_t i = hub[h];
     const int64_t sl = wide[i];
-    const int rows = sell_rows(sl, c, n_rows);
+    if (l >= sell_rows(sl, c, n_rows)) continue;
     const int32_t p0 = first_piece[i], p1 = i + 1 < n_wide ? first_piece[i + 1] : static_cast<int32_t>(n_pieces);
-    if (p1 - p0 <= 32) {
-      for (int l = lane; l < rows; l += 32) {
-        double sum = 0.0;
-        for (int32_t pc = p0; pc < p1; ++pc) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
-        store(sl, l, sum);
-      }
-    } else {
-      for (int l = 0; l < rows; ++l) {
-        double sum = 0.0;
-        for (int32_t pc = p0 + lane; pc < p1; pc += 32) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
-        sum = warp_sum(sum);
-        if (lane == 0) store(sl, l, sum);
-      }
+    double sum = 0.0;
+    for (int32_t pc = p0 + lane; pc < p1; pc += 32) sum += part[static_cast<int64_t>(pc) * SELL_PART_STRIDE + l];
+    sum = warp_sum(sum);
+    if (lane == 0) {
+      const int64_t p = sl * c + l;
+      const int64_t r = perm ? static_cast<int64_t>(perm[p]) : p;
+      y[r] = scale_p ? sc * sum : sum;
     }
   }
 }
@@ -273,9 +290,10 @@ namespace {
 // them, and those wide rows' sums.
 void sell_launch(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off, const int32_t* perm,
                  const int32_t* idx, const double* val, const int32_t* wide, int64_t n_wide,
-                 const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols, int64_t tail_from,
-                 int64_t max_narrow_width, const double* x, double* y, const double* scale, int64_t s_begin,
-                 int64_t s_end, int64_t i_begin, int64_t i_end, int64_t pc_begin, int64_t pc_end, cudaStream_t s) {
+                 const int32_t* first_piece, int64_t n_pieces, const int32_t* hub, int64_t n_hub, int64_t wide_cols,
+                 int64_t tail_from, int64_t max_narrow_width, const double* x, double* y, const double* scale,
+                 int64_t s_begin, int64_t s_end, int64_t i_begin, int64_t i_end, int64_t pc_begin, int64_t pc_end,
+                 int64_t h_begin, int64_t h_end, cudaStream_t s) {
   if (wide_cols <= 0) wide_cols = SPMVB_SELL_WIDE_COLS;
   if (tail_from < 0 || tail_from > n_rows) tail_from = n_rows;
   const int64_t p_begin = s_begin * c, p_end = s_end * c < n_rows ? s_end * c : n_rows;
@@ -298,9 +316,15 @@ void sell_launch(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t
                n_wide, first_piece, n_pieces, widths, slice_off, idx, val, x, part.get(),
                static_cast<int32_t>(pc_begin), static_cast<int32_t>(pc_end));
     SPMVB_LAUNCHED("k_sell_wide_part");
-    launch_pdl(k_sell_wide_final, dim3(grid_for((i_end - i_begin) * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows,
-               c, wide, n_wide, first_piece, n_pieces, part.get(), perm, y, scale, i_begin, i_end);
+    launch_pdl(k_sell_wide_final, dim3(grid_for((i_end - i_begin) * c, 256, 148 * 16)), dim3(256), 0, s, n_rows, c,
+               wide, n_wide, first_piece, n_pieces, part.get(), perm, y, scale, i_begin, i_end);
     SPMVB_LAUNCHED("k_sell_wide_final");
+    if (h_end > h_begin) {
+      if (!hub || h_end > n_hub) fail(SPMVB_INVALID_ARG, "hub slice list missing");
+      launch_pdl(k_sell_wide_hub, dim3(grid_for((h_end - h_begin) * c * 32, 256, 148 * 16)), dim3(256), 0, s, n_rows,
+                 c, wide, n_wide, first_piece, n_pieces, hub, part.get(), perm, y, scale, h_begin, h_end);
+      SPMVB_LAUNCHED("k_sell_wide_hub");
+    }
   }
 }
 
@@ -308,32 +332,33 @@ void sell_launch(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t
 
 extern "C" int spmvb_spmv_sell(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
-                               int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
-                               int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
-                               const double* scale, void* stream) {
+                               int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, const int32_t* hub,
+                               int64_t n_hub, int64_t wide_cols, int64_t tail_from, int64_t max_narrow_width,
+                               const double* x, double* y, const double* scale, void* stream) {
   return guard([&] {
     if (n_rows <= 0) return;
-    sell_launch(n_rows, c, widths, slice_off, perm, idx, val, wide, n_wide, first_piece, n_pieces, wide_cols,
-                tail_from, max_narrow_width, x, y, scale, 0, (n_rows + c - 1) / c, 0, n_wide, 0, n_pieces,
-                as_stream(stream));
+    sell_launch(n_rows, c, widths, slice_off, perm, idx, val, wide, n_wide, first_piece, n_pieces, hub, n_hub,
+                wide_cols, tail_from, max_narrow_width, x, y, scale, 0, (n_rows + c - 1) / c, 0, n_wide, 0,
+                n_pieces, 0, n_hub, as_stream(stream));
   });
 }
 
 extern "C" int spmvb_spmv_sell_range(int64_t n_rows, int64_t c, const int64_t* widths, const int64_t* slice_off,
                                      const int32_t* perm, const int32_t* idx, const double* val, const int32_t* wide,
-                                     int64_t n_wide, const int32_t* first_piece, int64_t n_pieces, int64_t wide_cols,
-                                     int64_t tail_from, int64_t max_narrow_width, const double* x, double* y,
-                                     const double* scale, int64_t s_begin, int64_t s_end, int64_t i_begin,
-                                     int64_t i_end, int64_t pc_begin, int64_t pc_end, void* stream) {
+                                     int64_t n_wide, const int32_t* first_piece, int64_t n_pieces,
+                                     const int32_t* hub, int64_t n_hub, int64_t wide_cols, int64_t tail_from,
+                                     int64_t max_narrow_width, const double* x, double* y, const double* scale,
+                                     int64_t s_begin, int64_t s_end, int64_t i_begin, int64_t i_end, int64_t pc_begin,
+                                     int64_t pc_end, int64_t h_begin, int64_t h_end, void* stream) {
   return guard([&] {
     if (n_rows <= 0) return;
     const int64_t n_slices = (n_rows + c - 1) / c;
     if (s_begin < 0 || s_end < s_begin || s_end > n_slices || i_begin < 0 || i_end < i_begin || i_end > n_wide ||
-        pc_begin < 0 || pc_end < pc_begin || pc_end > n_pieces)
-      fail(SPMVB_INVALID_ARG, "slice / wide-slice / piece range out of bounds");
-    sell_launch(n_rows, c, widths, slice_off, perm, idx, val, wide, n_wide, first_piece, n_pieces, wide_cols,
-                tail_from, max_narrow_width, x, y, scale, s_begin, s_end, i_begin, i_end, pc_begin, pc_end,
-                as_stream(stream));
+        pc_begin < 0 || pc_end < pc_begin || pc_end > n_pieces || h_begin < 0 || h_end < h_begin || h_end > n_hub)
+      fail(SPMVB_INVALID_ARG, "slice / wide-slice / piece / hub range out of bounds");
+    sell_launch(n_rows, c, widths, slice_off, perm, idx, val, wide, n_wide, first_piece, n_pieces, hub, n_hub,
+                wide_cols, tail_from, max_narrow_width, x, y, scale, s_begin, s_end, i_begin, i_end, pc_begin, pc_end,
+                h_begin, h_end, as_stream(stream));
   });
 }
 

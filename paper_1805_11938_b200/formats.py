@@ -65,6 +65,9 @@ class FormatTag(str, Enum):
     HYB = "hyb"
 
 
+SELL_HUB_PIECES = 32  # include/spmvb.h SPMVB_SELL_HUB_PIECES
+
+
 def _i32(n, dev):
     return torch.empty(int(n), dtype=torch.int32, device=dev)
 
@@ -313,19 +316,31 @@ class SellMatrix:
                 check(LIB.spmvb_sell_wide_plan(self.n_rows, self.c, ptr(self.widths), wide_cols, ptr(lst),
                                                ctypes.byref(cnt), ctypes.byref(mx), ptr(first),
                                                ctypes.byref(npieces), _lib.stream(self.device)))
-            self._wide = (lst, int(cnt.value), int(mx.value), first, int(npieces.value), wide_cols,
-                          self._empty_tail())
+            n_wide, n_pieces = int(cnt.value), int(npieces.value)
+            hub = _i32(1, self.device)
+            n_hub = 0
+            if n_wide:  # wide slices of more than SPMVB_SELL_HUB_PIECES (32) pieces: summed a warp per row
+                ends = torch.cat([first[1:n_wide].long(),
+                                  torch.tensor([n_pieces], dtype=torch.int64, device=self.device)])
+                hubs = torch.nonzero(ends - first[:n_wide].long() > SELL_HUB_PIECES).flatten().to(torch.int32)
+                n_hub = int(hubs.numel())
+                if n_hub:
+                    hub = hubs
+            self._wide = (lst, n_wide, int(mx.value), first, n_pieces, wide_cols, self._empty_tail(), hub, n_hub)
         return self._wide
 
     def range_plan(self, k: int):
         """About ``k`` slice ranges of roughly equal cells, aligned to the
         sigma sorting windows (so each range's rows are one contiguous block
         of y): a list of (s_begin, s_end, i_begin, i_end, pc_begin, pc_end,
-        row_begin, row_end) for ``kernels.spmv_sell_range``; cached."""
+        row_begin, row_end, h_begin, h_end) for ``kernels.spmv_sell_range``;
+        cached."""
         key = int(k)
         if key in self._ranges:
             return self._ranges[key]
         wide, n_wide, _, first, n_pieces = self.wide_plan()[:5]
+        hub, n_hub = self.wide_plan()[7:9]
+        hl = hub[:n_hub].cpu().numpy() if n_hub else np.empty(0, np.int32)
         S = self.n_slices
         align = max(self.sigma // self.c, 1) if self.sigma > 0 else 1
         off = self.slice_off.cpu().numpy()
@@ -345,7 +360,8 @@ class SellMatrix:
             i0, i1 = int(np.searchsorted(wl, s0)), int(np.searchsorted(wl, s1))
             pc0 = int(fp[i0]) if i0 < n_wide else n_pieces
             pc1 = int(fp[i1]) if i1 < n_wide else n_pieces
-            plan.append((s0, s1, i0, i1, pc0, pc1, s0 * self.c, min(s1 * self.c, self.n_rows)))
+            h0, h1 = int(np.searchsorted(hl, i0)), int(np.searchsorted(hl, i1))
+            plan.append((s0, s1, i0, i1, pc0, pc1, s0 * self.c, min(s1 * self.c, self.n_rows), h0, h1))
         self._ranges[key] = plan
         return plan
 

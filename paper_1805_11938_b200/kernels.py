@@ -275,11 +275,11 @@ def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
 
 
 def _args_sell(m: SellMatrix, xd, y, sp, scratch):
-    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from = m.wide_plan()
+    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from, hub, n_hub = m.wide_plan()
     perm = m.perm if m.sigma > 0 else None
     return "spmvb_spmv_sell", (m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices),
-                               ptr(m.flat_data), ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, tail_from,
-                               max_narrow, ptr(xd), ptr(y), sp)
+                               ptr(m.flat_data), ptr(wide), n_wide, ptr(first_piece), n_pieces, ptr(hub), n_hub,
+                               wide_cols, tail_from, max_narrow, ptr(xd), ptr(y), sp)
 
 
 def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
@@ -303,14 +303,16 @@ def spmv_sell_range(m: SellMatrix, x: torch.Tensor, out: torch.Tensor, r, *, sca
     if not xd.is_cuda or xd.dtype != torch.float64 or xd.numel() != m.n_cols:
         raise ValueError(f"x must be a float64 CUDA tensor of length {m.n_cols}")
     y = _out(m, out)
-    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from = m.wide_plan()
+    wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from, hub, n_hub = m.wide_plan()
     perm = m.perm if m.sigma > 0 else None
     s0, s1, i0, i1, pc0, pc1 = (int(v) for v in r[:6])
+    h0, h1 = int(r[8]), int(r[9])
     with torch.cuda.device(m.device):
         check(LIB.spmvb_spmv_sell_range(
             m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
-            ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, tail_from, max_narrow, ptr(xd.contiguous()),
-            ptr(y), ptr(scale) if scale is not None else None, s0, s1, i0, i1, pc0, pc1, _lib.stream(m.device)))
+            ptr(wide), n_wide, ptr(first_piece), n_pieces, ptr(hub), n_hub, wide_cols, tail_from, max_narrow,
+            ptr(xd.contiguous()), ptr(y), ptr(scale) if scale is not None else None, s0, s1, i0, i1, pc0, pc1, h0, h1,
+            _lib.stream(m.device)))
     return y
 
 
@@ -423,12 +425,12 @@ def bind_range(tag: FormatTag, m: FormatMatrix, x: torch.Tensor, out: torch.Tens
                 m.n_nonempty, ptr(carry), ptr(x), ptr(out), sp, t0, t1, a, b)
         return BoundCall("spmvb_spmv_csr5_tiles", args, st, keep=(m, x, out, scale, carry))
     if tag is FormatTag.SELL and isinstance(m, SellMatrix):
-        wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from = m.wide_plan()
+        wide, n_wide, max_narrow, first_piece, n_pieces, wide_cols, tail_from, hub, n_hub = m.wide_plan()
         perm = m.perm if m.sigma > 0 else None
         s0, s1, i0, i1, pc0, pc1 = (int(v) for v in r[:6])
         args = (m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices), ptr(m.flat_data),
-                ptr(wide), n_wide, ptr(first_piece), n_pieces, wide_cols, tail_from, max_narrow, ptr(x), ptr(out), sp,
-                s0, s1, i0, i1, pc0, pc1)
+                ptr(wide), n_wide, ptr(first_piece), n_pieces, ptr(hub), n_hub, wide_cols, tail_from, max_narrow,
+                ptr(x), ptr(out), sp, s0, s1, i0, i1, pc0, pc1, int(r[8]), int(r[9]))
         return BoundCall("spmvb_spmv_sell_range", args, st, keep=(m, x, out, scale))
     raise ValueError(f"row ranges exist for csr5 and sell matrices, not {tag.value!r} / {type(m).__name__}")
 

@@ -238,7 +238,7 @@ def test_c5_shadow_layout_spmv_sampled_rows(c5, y_ref, tag, kw):
     order = sp.DegreeOrder(c5["m"])
     rm = sp.convert(tag, order.matrix(c5["m"]), **kw)
     if tag == "sell":
-        _, n_wide, _, _, _, wide_cols, tail_from = rm.wide_plan()
+        _, n_wide, _, _, _, wide_cols, tail_from = rm.wide_plan()[:7]
         assert wide_cols == 4096 and n_wide > 0 and tail_from == -(-order.n_nonempty // 32) * 32
     y = order.to_old(sp.spmv(tag, rm, order.to_new(c5["x"])))
     got = h(y[torch.from_numpy(rows).cuda()])
