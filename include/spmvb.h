@@ -367,12 +367,14 @@ int spmvb_dist_destroy(spmvb_dist* d);
 /* The version (NCCL_VERSION_CODE) of the libnccl.so.2 the dist entry points
  * resolved: it must be the one that created the caller's communicator. */
 int spmvb_dist_nccl_version(int* version);
-/* The same step with the exchange overlapped: the shard is computed as
- * n_ranges row ranges (spans: world * n_ranges * 2 local row bounds [a, b)
- * of every rank's ranges, the same array on every rank; empty = a == b), and
- * each range's rows are sent to the peers on an internal exchange stream
- * while the next range computes.  range_spmv(ctx, k, x, y_local, scale,
- * stream) computes this rank's range k into y_local (the shard's rows).
+/* The same step with the exchange overlapped: range_spmv(ctx, k, x,
+ * y_local, scale, stream) is called for k = 0 .. n_ranges-1 in order and
+ * computes this rank's range k into y_local (the shard's rows; a no-op for
+ * a k past its own ranges); after each call the rows spans[rank][k] = local
+ * [a, b) are sent to every peer (and each peer's spans[p][k] received) on an
+ * internal exchange stream while the next range computes.  spans: world *
+ * n_ranges * 2, the same array on every rank; a == b sends nothing (rows
+ * known to be zero, e.g. an empty tail, need not travel).
  * Range bounds must not split a row's computation (e.g. CSR5 range_plan,
  * SELL range_plan); then x_next is the same, bit for bit, as spmvb_dist_step. */
 typedef int (*spmvb_range_spmv_fn)(void* ctx, int k, const double* x, double* y_local, const double* scale,

@@ -181,7 +181,9 @@ extern "C" int spmvb_dist_step_ranges(spmvb_dist* d, spmvb_range_spmv_fn range_s
     for (int k = 0; k < K; ++k) {
       int64_t a, b;
       span(me, k, a, b);
-      if (b > a) forward(range_spmv(ctx, k, x, x_next + lo, scale, stream));
+      // every k is computed (the callback knows its own ranges); the spans
+      // only say which rows travel (a range in the empty tail sends none)
+      forward(range_spmv(ctx, k, x, x_next + lo, scale, stream));
       if (d->world == 1) continue;
       SPMVB_CUDA(cudaEventRecord(d->events[k], s));
       SPMVB_CUDA(cudaStreamWaitEvent(cs, d->events[k], 0));

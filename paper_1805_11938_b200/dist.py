@@ -158,7 +158,7 @@ class PowerIteration:
     def __init__(self, local_spmv: Callable, bounds, rank: int, world: int, device: torch.device,
                  x0: torch.Tensor, group=None, ops=None, exchange: str = "allgatherv",
                  local_cols: torch.Tensor | None = None, local_ranges=None, local_spmv_range: Callable | None = None,
-                 local_spmv_push: Callable | None = None):
+                 local_spmv_push: Callable | None = None, send_rows: int | None = None):
         if exchange not in ("allgatherv", "sparse", "p2p"):
             raise ValueError(f"unknown exchange {exchange!r}")
         if exchange == "p2p" and world > 1 and dist.get_backend(group) == dist.Backend.GLOO:
@@ -201,6 +201,21 @@ class PowerIteration:
         self._fast = None
         self._fast_ok = (world == 1 and self.exchange == "allgatherv" and device.type == "cuda"
                          and hasattr(local_spmv, "bind") and self.ops is GpuOps)
+        # send_rows: this rank's rows past the first send_rows are empty, so
+        # their entries of every iterate after the first are exactly 0 -- the
+        # all-gatherv moves only each rank's leading send_rows rows and the
+        # peers' empty tails are zeroed once (a degree-ordered shard: C5 has
+        # 58 % empty rows)
+        self._send_hi = list(self.bounds[1:])
+        self._tails_pending = False
+        if world > 1 and self.exchange == "allgatherv":
+            mine = self.hi if send_rows is None else self.lo + min(max(int(send_rows), 0), self.hi - self.lo)
+            allhi = [None] * world
+            dist.all_gather_object(allhi, mine, group=self.group)
+            self._send_hi = [int(v) for v in allhi]
+            if self._send_hi != self.bounds[1:]:
+                self._zero_remote_tails(self.x_next)
+                self._tails_pending = True  # x (still x0) gets its remote tails zeroed after the first step
         self._spans = None
         if local_ranges is not None and world > 1 and self.exchange == "allgatherv":
             if local_spmv_range is None:
@@ -215,6 +230,18 @@ class PowerIteration:
             self._spans = allspans
 
     # ---- full exchange ---------------------------------------------------
+    def _zero_remote_tails(self, buf: torch.Tensor) -> None:
+        for p in range(self.world):
+            if p != self.rank and self._send_hi[p] < self.bounds[p + 1]:
+                buf[self._send_hi[p]:self.bounds[p + 1]].zero_()
+
+    def _after_step(self) -> None:
+        """Called after the swap: the first time, the old x0 buffer (now
+        x_next) still holds x0 in the peers' empty tails; zero them."""
+        if self._tails_pending:
+            self._zero_remote_tails(self.x_next)
+            self._tails_pending = False
+
     def _all_reduce_sumsq(self) -> None:
         if self._staged:
             s = self.sumsq.cpu()
@@ -225,23 +252,23 @@ class PowerIteration:
 
     def _allgatherv(self, y_full: torch.Tensor) -> None:
         if self._staged:  # exchange host copies, then upload the peers' rows
-            self._host[self.lo:self.hi].copy_(y_full[self.lo:self.hi])
+            self._host[self.lo:self._send_hi[self.rank]].copy_(y_full[self.lo:self._send_hi[self.rank]])
             self._allgatherv_tensor(self._host)
             for p in range(self.world):
-                lo, hi = self.bounds[p], self.bounds[p + 1]
+                lo, hi = self.bounds[p], self._send_hi[p]
                 if p != self.rank and hi > lo:
                     y_full[lo:hi].copy_(self._host[lo:hi])
             return
         self._allgatherv_tensor(y_full)
 
     def _allgatherv_tensor(self, y_full: torch.Tensor) -> None:
-        mine = y_full[self.lo : self.hi]
+        mine = y_full[self.lo : self._send_hi[self.rank]]
         ops = []
         for p in range(self.world):
             if p == self.rank:
                 continue
-            lo, hi = self.bounds[p], self.bounds[p + 1]
-            if self.hi > self.lo:
+            lo, hi = self.bounds[p], self._send_hi[p]
+            if mine.numel():
                 ops.append(dist.P2POp(dist.isend, mine, p, group=self.group))
             if hi > lo:
                 ops.append(dist.P2POp(dist.irecv, y_full[lo:hi], p, group=self.group))
@@ -328,10 +355,15 @@ class PowerIteration:
         # staged (gloo): each finished span is copied to the host and sent
         # from there; received spans are uploaded after the last wait
         buf = self._host if self._staged else self.x_next
+
+        def clip(p, span):  # the part of a span that is sent (rows before the empty tail)
+            return None if span is None else (span[0], max(span[0], min(span[1], self._send_hi[p])))
+
         reqs = []
         for k in range(max(len(sp) for sp in self._spans)):
-            mine = self._spans[me][k] if k < len(self._spans[me]) else None
-            if mine is not None:
+            full = self._spans[me][k] if k < len(self._spans[me]) else None
+            mine = clip(me, full)
+            if full is not None:
                 self.local_spmv_range(k, self.x, out, self.scale)
                 if self._staged and mine[1] > mine[0]:
                     buf[mine[0]:mine[1]].copy_(self.x_next[mine[0]:mine[1]])
@@ -341,7 +373,7 @@ class PowerIteration:
                     continue
                 if mine is not None and mine[1] > mine[0]:
                     ops.append(dist.P2POp(dist.isend, buf[mine[0]:mine[1]], p, group=self.group))
-                theirs = self._spans[p][k] if k < len(self._spans[p]) else None
+                theirs = clip(p, self._spans[p][k] if k < len(self._spans[p]) else None)
                 if theirs is not None and theirs[1] > theirs[0]:
                     ops.append(dist.P2POp(dist.irecv, buf[theirs[0]:theirs[1]], p, group=self.group))
             if ops:
@@ -352,11 +384,12 @@ class PowerIteration:
             r.wait()
         if self._staged:
             for p in range(self.world):
-                lo, hi = self.bounds[p], self.bounds[p + 1]
+                lo, hi = self.bounds[p], self._send_hi[p]
                 if p != me and hi > lo:
                     self.x_next[lo:hi].copy_(buf[lo:hi])
         self.ops.inv_sqrt(self.sumsq, self.scale)
         self.x, self.x_next = self.x_next, self.x
+        self._after_step()
 
     # ---- peer-memory exchange (our kernels over NVLink, no NCCL) ----------
     def _plan_p2p(self, x0: torch.Tensor, n: int) -> None:
@@ -473,6 +506,7 @@ class PowerIteration:
                 self._allgatherv(self.x_next)
         self.ops.inv_sqrt(self.sumsq, self.scale)
         self.x, self.x_next = self.x_next, self.x
+        self._after_step()
 
     def gather_full(self) -> torch.Tensor:
         """The whole current iterate on every rank (one all-gatherv; a no-op
@@ -646,7 +680,8 @@ class NativePowerIteration:
                             ctypes.c_void_p, ctypes.c_void_p)
 
     def __init__(self, local_op, bounds, rank: int, world: int, device: torch.device, x0: torch.Tensor,
-                 comm_ptr: int, ranges=None, range_op: Callable | None = None, group=None):
+                 comm_ptr: int, ranges=None, range_op: Callable | None = None, group=None,
+                 send_rows: int | None = None):
         self.bounds = [int(b) for b in bounds]
         self.rank, self.world, self.device = rank, world, device
         n = self.bounds[-1]
@@ -657,26 +692,34 @@ class NativePowerIteration:
         self.scale = torch.ones(1, dtype=torch.float64, device=device)
         pairs = ((self.x, self.x_next), (self.x_next, self.x))
         self._ranged = ranges is not None
+        # send_rows as in PowerIteration: only each rank's leading send_rows
+        # rows travel; the peers' empty tails are zeroed once
+        limit = hi - lo if send_rows is None else min(max(int(send_rows), 0), hi - lo)
         if self._ranged:
             if range_op is None:
                 raise ValueError("ranges need range_op")
             spans = [(int(a), int(b)) for a, b in ranges]
+            sent = [(a, max(a, min(b, limit))) for a, b in spans]
             allspans = [None] * world
             if world > 1:
-                dist.all_gather_object(allspans, spans, group=group)
+                dist.all_gather_object(allspans, (sent, lo + limit), group=group)
             else:
-                allspans = [spans]
-            K = max(len(sp_) for sp_ in allspans)
+                allspans = [(sent, lo + limit)]
+            self._send_hi = [int(h_) for _, h_ in allspans]
+            K = max(len(sp_) for sp_, _ in allspans)
             flat = []
-            for sp_ in allspans:
+            for sp_, _ in allspans:
                 sp_ = sp_ + [(0, 0)] * (K - len(sp_))
                 flat += [v for ab in sp_ for v in ab]
             self._calls = {(int(a.data_ptr()), k): range_op(k, a, b[lo:hi], self.scale) for a, b in pairs
                            for k in range(len(spans))}
 
             def local(ctx, k, x, y, scale, stream):
+                call = self._calls.get((int(x), int(k)))
+                if call is None:  # past this rank's own ranges
+                    return 0
                 try:
-                    self._calls[(int(x), int(k))]()
+                    call()
                     return 0
                 except Exception:  # reported through the status code
                     return _lib.SPMVB_INTERNAL
@@ -688,6 +731,9 @@ class NativePowerIteration:
             check(LIB.spmvb_dist_init_ranges(ctypes.c_void_p(comm_ptr), rank, world, b_arr, K, s_arr,
                                              ctypes.byref(h)))
         else:
+            if send_rows is not None:
+                raise ValueError("send_rows needs ranges (spmvb_dist_step_ranges)")
+            self._send_hi = list(self.bounds[1:])
             # the SpMV of each parity, bound once; the callback picks it by x
             self._calls = {int(a.data_ptr()): local_op.bind(a, b[lo:hi], self.scale) for a, b in pairs}
 
@@ -703,8 +749,16 @@ class NativePowerIteration:
             h = ctypes.c_void_p()
             check(LIB.spmvb_dist_init(ctypes.c_void_p(comm_ptr), rank, world, b_arr, ctypes.byref(h)))
         self._h = h
+        self._tails_pending = self._send_hi != self.bounds[1:]
+        if self._tails_pending:
+            self._zero_tails(self.x_next)
         self.exchange = "allgatherv"
         self.driver = "c-abi spmvb_dist_step" + ("_ranges" if self._ranged else "")
+
+    def _zero_tails(self, buf: torch.Tensor) -> None:
+        for p in range(self.world):
+            if p != self.rank and self._send_hi[p] < self.bounds[p + 1]:
+                buf[self._send_hi[p]:self.bounds[p + 1]].zero_()
 
     def step(self) -> None:
         fn = LIB.spmvb_dist_step_ranges if self._ranged else LIB.spmvb_dist_step
@@ -712,6 +766,9 @@ class NativePowerIteration:
             check(fn(self._h, ctypes.cast(self._cb, ctypes.c_void_p), None, ptr(self.x), ptr(self.x_next),
                      ptr(self.sumsq), ptr(self.scale), _lib.stream(self.device)))
         self.x, self.x_next = self.x_next, self.x
+        if self._tails_pending:  # the old x0 buffer still holds x0 in the peers' empty tails
+            self._zero_tails(self.x_next)
+            self._tails_pending = False
 
     def eigenvalue_estimate(self) -> float:
         s = float(self.scale.item())

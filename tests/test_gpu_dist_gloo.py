@@ -154,3 +154,65 @@ def test_gloo_overlapped_ranges_bit_identical(cuda):
     for rank in range(2):
         assert a[rank][0].tobytes() == b[rank][0].tobytes()
         assert a[rank][2] == b[rank][2]
+
+
+def _dealt_worker(rank, world, port_no, steps, out, tag, n_ranges):
+    """The N > 1 headline layout: DegreeOrder(parts=world) dealt row blocks,
+    each rank sending only its non-empty prefix (send_rows); the iterate is
+    mapped back to the original ids."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_1805_11938_b200 as sp
+    from paper_1805_11938_b200 import dist as spdist
+
+    (hr, hc, hv), _, n = _host_matrix()
+    dev = torch.device("cuda", 0)
+    csr = sp.to_csr(sp.canonicalize(hr, hc, hv, n, n, device=dev))
+    order = sp.DegreeOrder(csr, parts=world)
+    mat = order.matrix(csr)
+    bounds = order.part_bounds
+    lo, hi = bounds[rank], bounds[rank + 1]
+    shard = spdist.row_block(mat, lo, hi)
+    rowdeg = torch.diff(shard.ptr)
+    send_rows = int((rowdeg > 0).sum().item())
+    assert bool((rowdeg[:send_rows] > 0).all()) and bool((rowdeg[send_rows:] == 0).all())
+    kw = {"csr5": dict(omega=32, sigma=8), "sell": dict(sell_c=32, sell_sigma=0)}[tag]
+    m = sp.convert(tag, shard, **kw)
+    ranges, range_fn = None, None
+    if n_ranges:
+        if tag == "sell":
+            plan = m.range_plan(n_ranges)[::-1]
+            ranges = [(r_[6], r_[7]) for r_ in plan]
+        else:
+            tb, rb = m.range_plan(n_ranges)
+            k_all = len(tb) - 1
+            plan = [(int(rb[k]), int(rb[k + 1]) if k + 1 < k_all else m.n_rows, int(tb[k]), int(tb[k + 1]))
+                    for k in range(k_all)][::-1]
+            ranges = [(a, b) for a, b, _, _ in plan]
+
+        def range_fn(k, x, out_view, scale):
+            sp.bind_range(tag, m, x, out_view, plan[k], scale)()
+    x0 = order.to_new(torch.from_numpy(synth_ref.uniform(n, 7)).to(dev))
+    pi = spdist.PowerIteration(sp.SpmvOperator(tag, m), bounds, rank, world, dev, x0, local_ranges=ranges,
+                               local_spmv_range=range_fn, send_rows=send_rows)
+    for _ in range(STEPS):
+        pi.step()
+    out[rank] = (order.to_old(pi.gather_full()).cpu().numpy().copy(), float(pi.scale.item()), send_rows, hi - lo)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,tag,n_ranges", [(2, "sell", 3), (3, "csr5", 2), (2, "csr5", 0)])
+def test_gloo_dealt_layout_sends_only_nonempty_rows(cuda, world, tag, n_ranges):
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_dealt_worker, args=(world, _free_port(), STEPS, out, tag, n_ranges), nprocs=world, join=True)
+    want_x, want_scale = _serial(STEPS)
+    for rank in range(world):
+        full, scale, send_rows, rows = out[rank]
+        assert send_rows < rows  # there is an empty tail that did not travel
+        np.testing.assert_allclose(full, want_x, rtol=1e-9, atol=1e-12 * np.abs(want_x).max())
+        assert scale == pytest.approx(want_scale, rel=1e-12)
+    for rank in range(1, world):
+        assert out[rank][0].tobytes() == out[0][0].tobytes()

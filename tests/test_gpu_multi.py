@@ -67,6 +67,28 @@ def _worker(rank, world, port_no, out, exchange, fused):
             sp.spmv_csr5_push(m, x, o, peers, off, scale=s, carry=carry)
 
     x0 = synth_ref.uniform(n, 7)
+    if exchange == "native-dealt":  # the bench's N > 1 path: dealt shadow layout, C-ABI ranges, send_rows
+        order = sp.DegreeOrder(csr, parts=world)
+        mat = order.matrix(csr)
+        b = order.part_bounds
+        shard_d = spdist.row_block(mat, b[rank], b[rank + 1])
+        md = sp.to_sell(shard_d, 32, 0)
+        plan_d = md.range_plan(4)[::-1]
+        rowdeg = torch.diff(shard_d.ptr)
+        ne = int((rowdeg > 0).sum().item())
+        comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
+        pi = spdist.NativePowerIteration(
+            sp.SpmvOperator("sell", md), b, rank, world, dev, order.to_new(torch.from_numpy(x0).to(dev)), comm,
+            ranges=[(r_[6], r_[7]) for r_ in plan_d],
+            range_op=lambda k, xv, o, sc: sp.bind_range("sell", md, xv, o, plan_d[k], sc), send_rows=ne)
+        for _ in range(STEPS):
+            pi.step()
+        torch.cuda.synchronize()
+        out[rank] = (order.to_old(pi.x).cpu().numpy().copy(), float(pi.scale.item()))
+        pi.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if exchange == "native":  # the C ABI's spmvb_dist_* over torch's NCCL communicator
         comm = dist.group.WORLD._get_backend(dev)._comm_ptr()
         pi = spdist.NativePowerIteration(sp.SpmvOperator("csr5", m), bounds, rank, world, dev,
@@ -105,7 +127,7 @@ def _serial():
 
 
 @pytest.mark.parametrize("exchange,fused", [("allgatherv", False), ("sparse", False), ("p2p", True),
-                                            ("p2p", False), ("native", False)])
+                                            ("p2p", False), ("native", False), ("native-dealt", False)])
 def test_two_gpu_exchanges_match_serial(exchange, fused):
     out = mp.get_context("spawn").Manager().dict()
     mp.spawn(_worker, args=(2, _free_port(), out, exchange, fused), nprocs=2, join=True)
