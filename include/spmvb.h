@@ -271,9 +271,10 @@ int spmvb_spmv_csr5_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int3
 
 /* spmv_ell (kernels.py:98-116): per-row sequential accumulation over all k
  * slots (pads included), separately rounded products: bit-identical to the
- * reference kernel. */
-int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const double* x, double* y,
-                   const double* scale, void* stream);
+ * reference kernel.  n_cols: the length of x (its lines are prefetched into
+ * L2 with the first slot loads; 0 = no prefetch). */
+int spmvb_spmv_ell(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* idx, const double* val, const double* x,
+                   double* y, const double* scale, void* stream);
 
 /* spmv_sell (kernels.py:119-136); perm may be NULL for sigma == 0.  Slices
  * up to wide_cols (>= SPMVB_SELL_WIDE_COLS; 0 = that default) wide, or taller

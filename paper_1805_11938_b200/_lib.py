@@ -99,7 +99,7 @@ SIGNATURES: dict[str, tuple] = {
         [c_i64, c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, c_int,
          vp, vp, vp],
     ),
-    "spmvb_spmv_ell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp]),
+    "spmvb_spmv_ell": (c_int, [c_i64, c_i64, c_i64, vp, vp, vp, vp, vp, vp]),
     "spmvb_sell_wide_plan": (c_int, [c_i64, c_i64, vp, c_i64, vp, P_i64, P_i64, vp, P_i64, vp]),
     "spmvb_spmv_sell": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, c_i64, vp, c_i64, vp, c_i64, c_i64, c_i64,
                                 c_i64, vp, vp, vp, vp]),

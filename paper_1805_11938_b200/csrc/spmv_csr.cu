@@ -323,7 +323,7 @@ extern "C" int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx,
                               void* stream) {
   return guard([&] {
     if (tail_nnz == 0 && k > 0) {  // empty tail: the ELL part is the whole result
-      const int rc = spmvb_spmv_ell(n_rows, k, ell_idx, ell_val, x, y, scale, stream);
+      const int rc = spmvb_spmv_ell(n_rows, 0, k, ell_idx, ell_val, x, y, scale, stream);  // (no x length: no prefetch)
       if (rc != SPMVB_OK) fail(rc, "%s", spmvb_last_error());
       return;
     }

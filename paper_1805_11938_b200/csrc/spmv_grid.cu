@@ -12,10 +12,23 @@ namespace {
 // reference's sequential slot recurrence (bit-identical).  PF: the next four
 // slots' loads are in flight while the current four are summed (k >= 8);
 // without it more threads fit per SM (short rows).
+#ifndef SPMVB_ELL_PREFETCH_X
+#define SPMVB_ELL_PREFETCH_X 1
+#endif
 template <bool PF>
 __global__ void k_spmv_ell(int64_t n_rows, int64_t k, const int32_t* __restrict__ idx, const double* __restrict__ val,
-                           const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p) {
+                           const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ scale_p,
+                           int64_t n_cols) {
   pdl_wait();
+#if SPMVB_ELL_PREFETCH_X
+  // x into L2 alongside the first slot loads: the gathers that follow them
+  // then wait for L2, not for a second DRAM round trip (a one-wave kernel
+  // such as C1 is two dependent DRAM latencies long)
+  {
+    const int64_t line = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (line * 16 < n_cols) asm volatile("prefetch.global.L2 [%0];" ::"l"(x + line * 16));
+  }
+#endif
   const double s = load_scale(scale_p);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -269,16 +282,16 @@ extern "C" int spmvb_sell_wide_plan(int64_t n_rows, int64_t c, const int64_t* wi
   });
 }
 
-extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t k, const int32_t* idx, const double* val, const double* x,
-                              double* y, const double* scale, void* stream) {
+extern "C" int spmvb_spmv_ell(int64_t n_rows, int64_t n_cols, int64_t k, const int32_t* idx, const double* val,
+                              const double* x, double* y, const double* scale, void* stream) {
   return guard([&] {
     cudaStream_t s = as_stream(stream);
     if (n_rows <= 0) return;
     const dim3 g(grid_for(n_rows, 256)), b(256);
     // the prefetching slot loop from two full 4-slot steps on (C2, k = 8:
     // 24.6 -> 22.7 us L2-flushed); shorter rows keep the lighter loop
-    if (k >= 8) launch_pdl(k_spmv_ell<true>, g, b, 0, s, n_rows, k, idx, val, x, y, scale);
-    else launch_pdl(k_spmv_ell<false>, g, b, 0, s, n_rows, k, idx, val, x, y, scale);
+    if (k >= 8) launch_pdl(k_spmv_ell<true>, g, b, 0, s, n_rows, k, idx, val, x, y, scale, n_cols);
+    else launch_pdl(k_spmv_ell<false>, g, b, 0, s, n_rows, k, idx, val, x, y, scale, n_cols);
     SPMVB_LAUNCHED("k_spmv_ell");
   });
 }

@@ -261,7 +261,7 @@ def _spmv_csr5_host(m: Csr5Matrix, x, out, scale, ranges: int):
 
 
 def _args_ell(m: EllMatrix, xd, y, sp, scratch):
-    return "spmvb_spmv_ell", (m.n_rows, m.k, ptr(m.grid_indices), ptr(m.grid_data), ptr(xd), ptr(y), sp)
+    return "spmvb_spmv_ell", (m.n_rows, m.n_cols, m.k, ptr(m.grid_indices), ptr(m.grid_data), ptr(xd), ptr(y), sp)
 
 
 def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
