@@ -170,3 +170,47 @@ def test_guard_detects_an_overrun(guarded, sp):
         guarded.check()
     del y
     guarded.checked = 1
+
+
+def test_guarded_shadow_layout_paths(guarded, sp):
+    """The round-2 kernels under guard bands: SELL on a degree-ordered
+    matrix (empty-tail path, wide pieces incl. hub slices, slice ranges),
+    CSR5 sigma 8 at 5 blocks/SM with its ranges, ELL with the x prefetch,
+    the fused norm; all against the one-shot results / the oracle."""
+    from oracle import port, synth_ref
+
+    r, c, v = synth_ref.rmat(16, 16, 61)
+    n = 1 << 16
+    rng = np.random.default_rng(8)  # three rows of 40000 entries: a hub slice (> 32 pieces of 1024 columns)
+    hub_r = np.repeat(np.array([100, 2000, 30000]), 40000)
+    hub_c = np.concatenate([rng.choice(n, 40000, replace=False) for _ in range(3)])
+    row, col, val = port.canonicalize(np.concatenate([r, hub_r]), np.concatenate([c, hub_c]),
+                                      np.concatenate([v, rng.uniform(0.1, 1.0, hub_r.size)]), n, n)
+    a = sp.canonicalize(row, col, val, n, n)
+    order = sp.DegreeOrder(a)
+    shadow = order.matrix(a)
+    x = torch.from_numpy(synth_ref.uniform(n, 2)).cuda()
+    xp = order.to_new(x)
+    ref = port.dense_spmv_oracle(row, col, val, n, synth_ref.uniform(n, 2))
+    bound = port.dense_spmv_oracle(row, col, np.abs(val), n, np.abs(synth_ref.uniform(n, 2)))
+    for tag, kw in [("sell", dict(sell_c=32, sell_sigma=0)), ("csr5", dict(omega=32, sigma=8)),
+                    ("sell", dict(sell_c=4, sell_sigma=64))]:
+        m = sp.convert(tag, shadow, **kw)
+        if tag == "sell":
+            if kw["sell_c"] == 32:
+                assert m.wide_plan()[8] > 0  # hub slices exist
+            plan = m.range_plan(3)
+        else:
+            tb, rb = m.range_plan(3)
+            k = len(tb) - 1
+            plan = [(int(rb[i]), int(rb[i + 1]) if i + 1 < k else n, int(tb[i]), int(tb[i + 1])) for i in range(k)]
+        y = sp.spmv(tag, m, xp)
+        got = order.to_old(y).cpu().numpy()
+        assert np.all(np.abs(got - ref) <= 1e-12 * bound), tag
+        yr = torch.empty(n, dtype=torch.float64, device="cuda")
+        for rr in plan:
+            sp.bind_range(tag, m, xp, yr, rr)()
+        assert torch.equal(yr, y), tag
+    me = sp.to_ell(sp.synth.host_coo("C1"))
+    xe = sp.synth.uniform_vector(me.n_cols, 4)
+    assert torch.equal(sp.spmv("ell", me, xe), sp.spmv("ell", me, xe))
