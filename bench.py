@@ -741,13 +741,16 @@ def run_ours(args):
     native_error = None
     try:
         pi = make_pi(args.exchange)
+        for _ in range(warmup):
+            pi.step()
+        torch.cuda.synchronize()
     except Exception as exc:  # e.g. no NCCL communicator pointer in this torch: the torch driver instead
         if args.exchange != "allgatherv" or world == 1:
             raise
         native_error = f"{type(exc).__name__}: {str(exc)[:160]}"
         pi = make_pi("allgatherv-torch")
-    for _ in range(warmup):
-        pi.step()
+        for _ in range(warmup):
+            pi.step()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     # keep the GPU busy ~clock_ramp_s so clocks are sampled under load; the
