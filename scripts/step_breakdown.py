@@ -3,7 +3,7 @@ measures it (sustained load, CUDA events): blocks of K back-to-back SpMVs
 on the same x -> y, of K ping-pong SpMVs (x -> y -> x ...), of K fused
 norms, and of K full steps (PowerIteration fast path), interleaved after a
 2 s warm-up so all see the same (power-capped) clocks.  Layout and format
-as the headline: degree-ordered C5, SELL-32 sigma 8192 (or argv[1] = csr5).
+as the headline: degree-ordered C5, SELL-32 sigma 0 (or argv[1] = csr5).
 
     python scripts/step_breakdown.py [sell|csr5] > profiles/r02_step_breakdown.txt
 """
@@ -21,7 +21,7 @@ from paper_1805_11938_b200.relabel import DegreeOrder  # noqa: E402
 
 K = 40
 fmt = sys.argv[1] if len(sys.argv) > 1 else "sell"
-kw = dict(sell_c=32, sell_sigma=8192, max_cells=1 << 34) if fmt == "sell" else dict(omega=32, sigma=16)
+kw = dict(sell_c=32, sell_sigma=0, max_cells=1 << 34) if fmt == "sell" else dict(omega=32, sigma=16)
 dev = torch.device("cuda", 0)
 w = bench.WORKLOADS["C5"]
 csr = sp.to_csr(bench.build_workload(sp, synth, w, dev))
