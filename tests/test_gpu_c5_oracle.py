@@ -91,6 +91,9 @@ def host(c5):
     m4 = sp.to_csr5(m, 4, 16)
     wins[4] = _windows(h(m4.tile_ptr), m4.num_tiles, c5["n"])
     del m4
+    m8 = sp.to_csr5(m, 32, 8)
+    wins[(32, 8)] = _windows(h(m8.tile_ptr), m8.num_tiles, c5["n"])
+    del m8
     torch.cuda.empty_cache()
     ranges = sorted({(r0, r1) for w in wins.values() for _, _, r0, r1 in w})
     rows, ptr, ind, dat = _host(c5, ranges)
@@ -137,14 +140,14 @@ def test_c5_sampled_rows_bit_exact(c5, host):
         assert np.array_equal(gi, wi) and gd.tobytes() == wd.tobytes()
 
 
-@pytest.mark.parametrize("omega", [32, 4])
-def test_c5_csr5_tile_windows(c5, host, omega):
+@pytest.mark.parametrize("omega,sigma", [(32, 16), (4, 16), (32, 8)])
+def test_c5_csr5_tile_windows(c5, host, omega, sigma):
     sp, m = c5["sp"], c5["m"]
-    sigma, tile = 16, omega * 16
+    tile = omega * sigma
     m5 = sp.to_csr5(m, omega, sigma)
     T = m5.num_tiles
     dptr = h(m.ptr).astype(np.int64)
-    for t0, t1, r0, r1 in host["wins"][omega]:
+    for t0, t1, r0, r1 in host["wins"][omega if sigma == 16 else (omega, sigma)]:
         wptr, wind, wdat = _rows_of(host, np.arange(r0, r1))
         p0, p1 = t0 * tile, min(t1 * tile, m.nnz)
         o = p0 - int(dptr[r0])

@@ -80,7 +80,7 @@ def test_config_parity(sp, name):
     assert np.array_equal(h(m.ptr), ptr)
     check_within(sp.spmv("csr", m, xd), ref, bound)
 
-    for om, sg in [(4, 16), (32, 16)]:
+    for om, sg in [(4, 16), (32, 16), (32, 8)]:
         m5 = sp.to_csr5(m, om, sg)
         o5 = port.to_csr5(ptr, ind, dat, n, om, sg)
         for f in ("tile_ptr", "bit_flag", "y_off", "seg_off", "indices"):
