@@ -183,8 +183,9 @@ def select_format_measured(a, formats=None, *, params=None, reps: int = 10, warm
 
     tags = [FormatTag(f) for f in formats] if formats else list(FormatTag)
     params = params or MEASURED_CANDIDATES
-    x = torch.ones(a.n_cols, dtype=torch.float64, device=a.row.device)
-    y = torch.empty(a.n_rows, dtype=torch.float64, device=a.row.device)
+    dev = a.device  # a COO or a CSR matrix
+    x = torch.ones(a.n_cols, dtype=torch.float64, device=dev)
+    y = torch.empty(a.n_rows, dtype=torch.float64, device=dev)
     times, best = {}, None
     for tag in tags:
         try:

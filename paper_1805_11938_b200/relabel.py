@@ -168,24 +168,47 @@ class RelabelledMatrix:
         return self.order.to_old(self.spmv(self.order.to_new(x)))
 
 
-def power_iteration(a, x0, steps: int, tag="csr5", *, relabel: bool = True, graph: bool = False, **convert_kw):
+# the candidates tag="auto" times (the bench's shadow-layout candidates)
+AUTO_CANDIDATES = {
+    FormatTag.CSR: {},
+    FormatTag.CSR5: dict(omega=32, sigma=8),
+    FormatTag.SELL: dict(sell_c=32, sell_sigma=0, max_cells=1 << 34),
+    FormatTag.HYB: dict(max_cells=1 << 34),
+}
+
+
+def power_iteration(a, x0, steps: int, tag="auto", *, relabel: bool = True, graph: bool = False, **convert_kw):
     """``steps`` iterations of x <- A x / ||A x|| on one GPU; returns the
     unit-norm iterate and ``||A x_{k-1}||`` (the eigenvalue estimate), x in
     the original ids.  ``relabel`` runs them on the
     degree-ordered shadow layout (one permutation of x0 before, one of the
     result after); ``graph`` replays the steps from a CUDA graph
-    (dist.PowerIteration.run)."""
+    (dist.PowerIteration.run).  ``tag="auto"`` converts the matrix the steps
+    run on to each of AUTO_CANDIDATES, times one SpMV of each and keeps the
+    fastest (model.select_format_measured): SELL-32 on a degree-ordered
+    R-MAT, ELL/SELL on stencils."""
     from .dist import PowerIteration
+    from .model import select_format_measured
 
     csr = _as_csr(a)
     dev = csr.device
     x0 = torch.as_tensor(x0, dtype=torch.float64).to(dev).reshape(-1)
     if relabel:
-        rm = RelabelledMatrix(tag, csr, **convert_kw)
-        pi = PowerIteration(rm, [0, csr.n_rows], 0, 1, dev, rm.order.to_new(x0))
+        order = DegreeOrder(csr)
+        shadow = order.matrix(csr)
+        if tag == "auto":
+            tag, m, _ = select_format_measured(shadow, list(AUTO_CANDIDATES), params=AUTO_CANDIDATES)
+        else:
+            m = convert(tag, shadow, **convert_kw)
+        del shadow
+        pi = PowerIteration(SpmvOperator(tag, m), [0, csr.n_rows], 0, 1, dev, order.to_new(x0))
         pi.run(steps, graph=graph)
-        return rm.order.to_old(pi.normalized()), pi.eigenvalue_estimate()
-    m = convert(tag, csr, **convert_kw)
+        return order.to_old(pi.normalized()), pi.eigenvalue_estimate()
+    if tag == "auto":
+        cands = dict(AUTO_CANDIDATES, **{FormatTag.ELL: {}})
+        tag, m, _ = select_format_measured(csr, list(cands), params=cands)
+    else:
+        m = convert(tag, csr, **convert_kw)
     pi = PowerIteration(SpmvOperator(tag, m), [0, csr.n_rows], 0, 1, dev, x0)
     pi.run(steps, graph=graph)
     return pi.normalized(), pi.eigenvalue_estimate()

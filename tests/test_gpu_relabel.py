@@ -150,6 +150,11 @@ def test_relabelled_power_iteration_matches_oracle(sp):
     np.testing.assert_allclose(np_(x_rel), xo, rtol=1e-9, atol=1e-14)
     np.testing.assert_allclose(np_(x_pl), xo, rtol=1e-9, atol=1e-14)
     assert lam_rel == pytest.approx(lam, rel=1e-12) and lam_pl == pytest.approx(lam, rel=1e-12)
+    # tag="auto": the format timed fastest on the shadow layout (relabel) or the plain matrix
+    for rel in (True, False):
+        x_a, lam_a = sp.power_iteration(a, torch.from_numpy(x0).cuda(), steps, relabel=rel)
+        np.testing.assert_allclose(np_(x_a), xo, rtol=1e-9, atol=1e-14)
+        assert lam_a == pytest.approx(lam, rel=1e-12)
 
 
 def test_relabelled_spmv_at_c4(sp):
