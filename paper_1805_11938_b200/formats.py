@@ -283,11 +283,10 @@ class SellMatrix:
         """Slices up to this width are summed one thread per row (sequential,
         bit-identical); wider ones by a CTA per ~32K-cell piece.  256 (the
         header's SPMVB_SELL_WIDE_COLS) unless the matrix is big enough for
-        longer per-thread rows to hide behind the rest of the grid: about
-        twice the cells per resident thread, rounded up to a power of two,
-        at most 4096, and only if the wide slices are all in the first
-        quarter of the grid (degree-ordered C5: 2.20 -> 2.09 ms at 4096; C4
-        stays at 256, where 1024 would serialise it: 135 -> 222 us;
+        4096-slot per-thread rows to hide behind the rest of the grid (at
+        least ~1200 cells per resident thread) and its wide slices all come
+        first (degree-ordered C5: 2.20 -> 2.09 ms at 4096; C4 stays at 256,
+        where 1024 would serialise it: 135 -> 222 us;
         profiles/r02_sell_ab2.txt)."""
         w = 256
         wide = torch.nonzero(self.widths > w)
@@ -298,9 +297,11 @@ class SellMatrix:
             return w
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         per_thread = self.total_cells / max(sms * 2048, 1)
-        while w < 4096 and w < 2 * per_thread:
-            w *= 2
-        return w
+        # measured: the whole degree-ordered C5 (~1750 cells per resident
+        # thread) gains from 4096 (2.20 -> 2.09 ms); its dealt 1/2 .. 1/8
+        # shards (870 .. 220) do not, and 512 costs 1/8 a quarter
+        # (0.31 -> 0.39 ms, profiles/r02_sell_shard_wide_probe.txt)
+        return 4096 if per_thread >= 1200 else w
 
     def wide_plan(self):
         """(wide slice list, count, widest remaining slice, first piece per
