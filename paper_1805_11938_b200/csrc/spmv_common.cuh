@@ -8,8 +8,30 @@ namespace spmvb {
 #ifndef SPMVB_LDX_NOALLOC
 #define SPMVB_LDX_NOALLOC 0  // 1: x gathers bypass L1 allocation (A/B knob)
 #endif
+#ifndef SPMVB_LDX_HOT
+#define SPMVB_LDX_HOT 0  // > 0: columns >= this gather without L1 allocation (A/B knob)
+#endif
+#ifndef SPMVB_LDX_HOT_MODE
+#define SPMVB_LDX_HOT_MODE 0  // 0: cold no_allocate; 1: hot evict_last + cold evict_first
+#endif
 __device__ __forceinline__ double ldx(const double* __restrict__ x, int32_t j) {
-#if SPMVB_LDX_NOALLOC
+#if SPMVB_LDX_HOT > 0
+  double v;
+  if (j < SPMVB_LDX_HOT) {
+#if SPMVB_LDX_HOT_MODE == 1
+    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
+#else
+    v = __ldg(x + j);
+#endif
+  } else {
+#if SPMVB_LDX_HOT_MODE == 1
+    asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
+#else
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
+#endif
+  }
+  return v;
+#elif SPMVB_LDX_NOALLOC
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
   return v;

@@ -1,6 +1,6 @@
 """SELL SpMV timing for same-box A/B of library builds (SPMVB_LIB_PATH):
-SELL-32 sigma 8192 on the degree-ordered C5 and C4 (the power-iteration
-format there) and SELL-32 sigma 1024 on C3.  Prints time and a hash of y
+SELL-32 sigma 0 on the degree-ordered C5 (the power-iteration format
+there), its dealt 8-way shard 0 and C4, and SELL-32 sigma 1024 on C3.  Prints time and a hash of y
 (variants must agree bit for bit).
 
     for v in ab_libs/*.so; do SPMVB_LIB_PATH=$v python scripts/sell_ab.py; done
@@ -29,15 +29,21 @@ def main():
     dev = torch.device("cuda", 0)
     flush = torch.empty(1 << 26, dtype=torch.float64, device=dev)
     lib = Path(os.environ.get("SPMVB_LIB_PATH", "default")).stem
-    for cfg, relabel, kw in (("C5", True, dict(sell_c=32, sell_sigma=8192, max_cells=1 << 34)),
-                             ("C4", True, dict(sell_c=32, sell_sigma=8192, max_cells=1 << 34)),
+    for cfg, relabel, kw in (("C5", True, dict(sell_c=32, sell_sigma=0, max_cells=1 << 34)),
+                             ("C5/8", True, dict(sell_c=32, sell_sigma=0, max_cells=1 << 34)),
+                             ("C4", True, dict(sell_c=32, sell_sigma=0, max_cells=1 << 34)),
                              ("C3", False, dict(sell_c=32, sell_sigma=1024, max_cells=1 << 34))):
-        w = bench.WORKLOADS[cfg]
+        w = bench.WORKLOADS[cfg.split("/")[0]]
         csr = sp.to_csr(bench.build_workload(sp, synth, w, dev))
         x = synth.uniform_vector(csr.n_cols, w["x_seed"], device=dev)
         if relabel:
-            order = DegreeOrder(csr, key="row")
+            parts = int(cfg.split("/")[1]) if "/" in cfg else 1
+            order = DegreeOrder(csr, key="row", parts=parts)
             csr, x = order.matrix(csr), order.to_new(x)
+            if parts > 1:
+                from paper_1805_11938_b200 import dist as spdist
+
+                csr = spdist.row_block(csr, 0, order.part_bounds[1])
         m = sp.convert("sell", csr, **kw)
         y = torch.empty(m.n_rows, dtype=torch.float64, device=dev)
         fn = lambda: sp.spmv("sell", m, x, out=y)  # noqa: E731
@@ -45,7 +51,7 @@ def main():
             fn()
         times = []
         for _ in range(3):  # three rounds of 20 back-to-back (hot) or 10 flushed reps
-            if cfg == "C5":
+            if cfg.startswith("C5"):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
                 for _ in range(20):
