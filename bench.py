@@ -387,8 +387,16 @@ def run_configs(args, dev, peak, traffic):
             del order, shadow, xp, yp
         good = {k: v for k, v in recs.items() if "error" not in v}
         best = max(good, key=lambda k: good[k]["gflops"])
+        # the same clock around a launch that only writes y: event + launch +
+        # one DRAM round trip, which a one-wave SpMV (C1) cannot go below
+        t_floor = flushed_time(lambda: y.fill_(0.0), flush, reps=args.config_reps)
+        b_best = good[best]["bytes_model"]
+        t_best = good[best]["us"] * 1e-6
         entry = {"workload": w["desc"], "n": n, "nnz": nnz, "generate_s": t_gen, "best": best,
                  "best_gflops": good[best]["gflops"], "best_frac": good[best]["frac"],
+                 "launch_floor_us": t_floor * 1e6,
+                 "best_frac_above_floor": (b_best / max(t_best - t_floor, 1e-9) / 1e9 / peak
+                                           if t_best > t_floor else None),
                  "all_within_tol": all(v["within_tol"] for v in good.values()),
                  "formats": recs}
         if name == "C3":
