@@ -320,7 +320,7 @@ def run_configs(args, dev, peak, traffic):
     layout (relabel.py); C3 adds its 100-iteration power iteration replayed
     from a CUDA graph (flushed once before the 100 steps) and run eagerly."""
     import paper_1805_11938_b200 as sp
-    from paper_1805_11938_b200 import dist as spdist, synth
+    from paper_1805_11938_b200 import _lib, dist as spdist, synth
     from paper_1805_11938_b200.harness import spmv_bytes
     from paper_1805_11938_b200.relabel import DegreeOrder
 
@@ -340,6 +340,16 @@ def run_configs(args, dev, peak, traffic):
         csr = sp.to_csr(a)
         del a
         recs = {}
+        gpart = torch.empty(int(_lib.load().spmvb_gather_probe_threads()), dtype=torch.float64, device=dev)
+        stream_ptr = torch.cuda.current_stream(dev).cuda_stream
+
+        def dot_ceiling(c, xv):
+            """Flat dot product over c's entries (spmvb_dot_probe): the stream + gather ceiling, L2-flushed."""
+            return flushed_time(lambda: _lib.check(_lib.load().spmvb_dot_probe(
+                xv.data_ptr(), c.indices.data_ptr(), c.data.data_ptr(), c.nnz, gpart.data_ptr(), stream_ptr)),
+                flush, reps=args.config_reps)
+
+        t_dot = {"": dot_ceiling(csr, x)}
 
         def measure(label, fn, m_bytes, yv, convert_ms):
             t = flushed_time(fn, flush, reps=args.config_reps)
@@ -372,6 +382,7 @@ def run_configs(args, dev, peak, traffic):
             t_order = (time.perf_counter() - t0) * 1e3
             xp = order.to_new(x)
             yp = torch.empty_like(xp)
+            t_dot["-relabel"] = dot_ceiling(shadow, xp)
             for tag, kw in RUN_CANDIDATES:
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
@@ -397,12 +408,15 @@ def run_configs(args, dev, peak, traffic):
                  "launch_floor_us": t_floor * 1e6,
                  "best_frac_above_floor": (b_best / max(t_best - t_floor, 1e-9) / 1e9 / peak
                                            if t_best > t_floor else None),
+                 "stream_gather_ceiling_us": {("reference layout" if k == "" else "degree-ordered layout"): v * 1e6
+                                              for k, v in t_dot.items()},
+                 "best_frac_of_stream_gather_ceiling": t_dot["-relabel" if best.endswith("-relabel") else ""] / t_best,
                  "all_within_tol": all(v["within_tol"] for v in good.values()),
                  "formats": recs}
         if name == "C3":
             entry["power_iteration_100"] = c3_power_iteration(sp, spdist, csr, x, flush, nnz)
         out[name] = entry
-        del csr, x, y, ref, bound
+        del csr, x, y, ref, bound, gpart
         torch.cuda.empty_cache()
     del flush
     torch.cuda.empty_cache()
@@ -670,11 +684,28 @@ def run_ours(args):
                                                   gpart.data_ptr(), stream_ptr))
 
     t_gather = event_time(probe, reps=10)
+
+    # Stream + gather ceiling, measured live: the flat dot product
+    # sum val[i] * x[idx[i]] over this shard's entries -- the SpMV's own
+    # traffic with no row structure (spmvb_dot_probe), L2-flushed like the
+    # kernel when the shard is small
+    def dot_probe():
+        _lib.check(_lib.load().spmvb_dot_probe(x_run.data_ptr(), shard_run.indices.data_ptr(),
+                                               shard_run.data.data_ptr(), shard_run.nnz, gpart.data_ptr(),
+                                               stream_ptr))
+
+    t_dot = (flushed_time(dot_probe, flush, reps=10) if flush is not None else event_time(dot_probe, reps=10))
     del gpart
     gather = {"gathers_per_launch": int(m.nnz), "achieved_G_per_s": m.nnz / t_kernel / 1e9,
               "peak_G_per_s": shard_run.nnz / t_gather / 1e9,
               "frac": (m.nnz / t_kernel) / (shard_run.nnz / t_gather),
               "peak_source": "spmvb_gather_probe: x summed at all of this shard's column indices (CUDA events)"}
+    stream_gather = {"entries_per_launch": int(shard_run.nnz), "achieved_G_per_s": shard_run.nnz / t_kernel / 1e9,
+                     "peak_G_per_s": shard_run.nnz / t_dot / 1e9, "frac": t_dot / t_kernel,
+                     "peak_ms": t_dot * 1e3,
+                     "peak_source": "spmvb_dot_probe: the flat dot product sum val[i]*x[idx[i]] over this shard's "
+                                    "entries (12 streamed bytes + one x gather per entry, no row structure; CUDA "
+                                    "events" + (", L2-flushed)" if flush is not None else ")")}
 
     # ---- timed power iteration ----
     # (a single process binds its launches once per buffer parity: dist.PowerIteration fast path)
@@ -945,7 +976,7 @@ def run_ours(args):
                          "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0,
                          "reference_layout": {"variant": olabel, "frac": formats[olabel].get("frac"),
                                               "gflops": formats[olabel].get("gflops")},
-                         "gather_bound": gather},
+                         "gather_bound": gather, "stream_gather_bound": stream_gather},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -420,6 +420,13 @@ int spmvb_sum_inv_sqrt(const double* vals, int n, double* sumsq, double* scale, 
  * partial holds spmvb_gather_probe_threads() doubles. */
 int64_t spmvb_gather_probe_threads(void);
 int spmvb_gather_probe(const double* src, const int32_t* idx, int64_t n, double* partial, void* stream);
+/* The same with the values: partial[t] = sum of val[i] * src[idx[i]] -- the
+ * flat dot product over a matrix's entries, i.e. an SpMV's own traffic (12
+ * streamed bytes + one gather per entry) without any row structure.  The
+ * stream + gather ceiling of that matrix on this GPU (bench.py reports the
+ * SpMV against it). */
+int spmvb_dot_probe(const double* src, const int32_t* idx, const double* val, int64_t n, double* partial,
+                    void* stream);
 
 /* ======================================================================== */
 /* Features — replaces features.py:69-84 (extract_features)                 */

@@ -124,6 +124,7 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_sum_inv_sqrt": (c_int, [vp, c_int, vp, vp, vp]),
     "spmvb_gather_probe_threads": (c_i64, []),
     "spmvb_gather_probe": (c_int, [vp, vp, c_i64, vp, vp]),
+    "spmvb_dot_probe": (c_int, [vp, vp, vp, c_i64, vp, vp]),
     "spmvb_csr_features": (c_int, [c_i64, c_i64, c_i64, vp, P_dbl, vp]),
     "spmvb_csr_extra_features": (c_int, [c_i64, c_i64, vp, vp, P_dbl, vp]),
     "spmvb_rmat_begin": (c_int, [c_int, c_i64, c_dbl, c_dbl, c_dbl, c_u64, P_vp, P_i64, vp]),

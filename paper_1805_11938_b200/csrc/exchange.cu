@@ -78,6 +78,32 @@ __global__ void k_gather_sum(const double* __restrict__ src, const int32_t* __re
   partial[tid] = acc;
 }
 
+// Stream + gather probe: the flat dot product sum val[i] * src[idx[i]] -- an
+// SpMV's own traffic (12 streamed bytes and one x gather per entry) with no
+// row structure at all (no pointers, permutation, y stores or carries,
+// perfectly balanced).  An SpMV over the same entries cannot be faster.
+__global__ void k_dot_sum(const double* __restrict__ src, const int32_t* __restrict__ idx,
+                          const double* __restrict__ val, int64_t n, double* __restrict__ partial) {
+  constexpr int U = 8;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  double acc = 0.0;
+  int64_t i = tid;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    int32_t c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = ld_stream(idx + i + u * stride);
+      v[u] = ld_stream(val + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u] * __ldg(src + c[u]);
+  }
+  for (; i < n; i += stride) acc += val[i] * __ldg(src + idx[i]);
+  partial[tid] = acc;
+}
+
 // Rows [0, n) of src written into every peer buffer dst[p] + offset (peer
 // addresses mapped over NVLink, e.g. symmetric-memory buffers): 16-byte
 // vector stores where the alignment allows, one pass over src per launch.
@@ -164,6 +190,15 @@ extern "C" int spmvb_gather_probe(const double* src, const int32_t* idx, int64_t
     cudaStream_t s = as_stream(stream);
     k_gather_sum<<<148 * 8, 256, 0, s>>>(src, idx, n, partial);
     SPMVB_LAUNCHED("k_gather_sum");
+  });
+}
+
+extern "C" int spmvb_dot_probe(const double* src, const int32_t* idx, const double* val, int64_t n, double* partial,
+                               void* stream) {
+  return guard([&] {
+    cudaStream_t s = as_stream(stream);
+    k_dot_sum<<<148 * 8, 256, 0, s>>>(src, idx, val, n, partial);
+    SPMVB_LAUNCHED("k_dot_sum");
   });
 }
 

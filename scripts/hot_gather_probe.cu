@@ -66,6 +66,36 @@ __global__ void __launch_bounds__(1024, 1) k_hot_sum(const double* __restrict__ 
   partial[tid] = acc;
 }
 
+// mode 3: the SpMV's own traffic without its row structure: the flat dot
+// product sum val[i] * x[idx[i]] (12 streamed bytes + one gather per entry)
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <int U>
+__global__ void __launch_bounds__(1024, 1) k_dot(const double* __restrict__ src, const int32_t* __restrict__ idx,
+                                                 const double* __restrict__ val, int64_t n,
+                                                 double* __restrict__ partial) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  double acc = 0.0;
+  int64_t i = tid;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    int32_t c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c[u] = ld_stream_i32(idx + i + u * stride);
+      v[u] = ld_stream_f64(val + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u] * __ldg(src + c[u]);
+  }
+  for (; i < n; i += stride) acc += val[i] * __ldg(src + idx[i]);
+  partial[tid] = acc;
+}
+
 template <int U, int MODE>
 int launch(const double* src, const int32_t* idx, int64_t n, int32_t hot, int threads, int blocks, double* partial,
            cudaStream_t s) {
@@ -78,6 +108,15 @@ int launch(const double* src, const int32_t* idx, int64_t n, int32_t hot, int th
 }
 
 }  // namespace
+
+extern "C" int dot_probe(const double* src, const int32_t* idx, const double* val, int64_t n, int threads, int blocks,
+                         int u, double* partial, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (u == 4) k_dot<4><<<blocks, threads, 0, s>>>(src, idx, val, n, partial);
+  else if (u == 8) k_dot<8><<<blocks, threads, 0, s>>>(src, idx, val, n, partial);
+  else return -1;
+  return static_cast<int>(cudaGetLastError());
+}
 
 extern "C" int hot_probe(const double* src, const int32_t* idx, int64_t n, int32_t hot, int threads, int blocks,
                          int mode, int u, double* partial, void* stream) {

@@ -35,6 +35,9 @@ def build():
     lib.hot_probe.restype = ctypes.c_int
     lib.hot_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int,
                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    lib.dot_probe.restype = ctypes.c_int
+    lib.dot_probe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
     return lib
 
 
@@ -77,6 +80,20 @@ def main():
                                                                             part.data_ptr(), stream)))
             print(f"{cfg} {name:10s} n {n:>10d}  library probe (148x8 CTAs of 256, U16): {n / base / 1e9:7.1f} G/s "
                   f"({base * 1e6:8.1f} us)", flush=True)
+            if os.environ.get("HOT_PROBE_DOT"):
+                # the SpMV's traffic without its row structure: sum val[i] * x[idx[i]]
+                val = torch.rand(n, dtype=torch.float64, device=dev)
+                for threads, blocks in ((1024, sms), (512, 2 * sms), (256, 5 * sms), (256, 8 * sms)):
+                    for u in (4, 8):
+                        def rund():
+                            rc = lib.dot_probe(x.data_ptr(), idx.data_ptr(), val.data_ptr(), n, threads, blocks, u,
+                                               part.data_ptr(), stream)
+                            assert rc == 0, rc
+                        t = timed(rund)
+                        print(f"{cfg} {name:10s} flat dot product, {blocks} CTAs of {threads}, U {u}: "
+                              f"{n / t / 1e9:7.1f} G/s ({t * 1e6:8.1f} us)", flush=True)
+                del val
+                continue
             ref = None
             for threads in (512, 1024):
                 for u in (4, 8):
