@@ -843,41 +843,10 @@ def run_ours(args):
                 "sent_rows_rank0": send_rows if send_rows is not None else (hi - lo),
                 "shard_rows_rank0": hi - lo,
                 f"ms_per_step_{pi.exchange}": t_loop / args.steps * 1e3}
-    if world > 1:
-        # the other exchanges, same steps, for comparison (report
-        # the all-gather and the sparse exchange; p2p = our kernels over NVLink)
-        vol = getattr(pi, "exchange_volume", None)
-        mode = pi.exchange
-        native = hasattr(pi, "driver")
-        del pi
-        others = ["allgatherv", "sparse"] + (["p2p"] if args.compare_p2p else [])
-        if native:  # the C-ABI driver ran the headline: time the torch one beside it
-            others[0] = "allgatherv-torch"
-        for other in others:
-            if other == mode:
-                continue
-            try:
-                pj = make_pi(other)
-                for _ in range(warmup):
-                    pj.step()
-                dist.barrier()
-                torch.cuda.synchronize()
-                ev0.record()
-                for _ in range(args.steps):
-                    pj.step()
-                ev1.record()
-                torch.cuda.synchronize()
-                tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
-                coll(dist.all_reduce, tt, op=dist.ReduceOp.MAX)
-                exchange[f"ms_per_step_{other}"] = float(tt.item()) / args.steps * 1e3
-                vol = vol or getattr(pj, "exchange_volume", None)
-                del pj
-            except Exception as exc:  # e.g. symmetric memory unavailable: report, keep the run
-                exchange[f"error_{other}"] = f"{type(exc).__name__}: {str(exc)[:160]}"
-        if vol:
-            exchange["rank0_volume_entries"] = vol
-    else:
-        del pi
+    mode = pi.exchange
+    native = hasattr(pi, "driver")
+    vol = getattr(pi, "exchange_volume", None)
+    del pi
 
     # ---- end to end through the public API with host buffers ----
     # Headline: a dependent chain of single calls on the reference-layout
@@ -951,44 +920,95 @@ def run_ours(args):
                "cpu": cpu_baseline.cpu_model(), "host_build_s": t_build}
         del ptr_h, ind, dat
 
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": warmup, "ms_per_step": t_loop / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": w["desc"], "format": tag, "variant": label,
+                   "params": {k: v for k, v in kw.items() if k != "max_cells"}, "n": n,
+                   "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
+                   "balance": ("degree-sorted rows dealt round-robin to the rank blocks (nnz-balanced to "
+                               "within one row)" if relabel and world > 1 else args.balance),
+                   "layout": ("degree-ordered shadow P A P^T (relabel.py), iterate x' = P x; the reference-layout "
+                              "matrix serves the e2e calls" if relabel else "reference layout"),
+                   "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"
+                            if world > 1 else "y=s*A x; ||y||^2; s=1/||y||"),
+                   "eigenvalue_estimate": eig,
+                   "l2": (f"inputs larger than L2 ({bytes_model / 1e6:.0f} MB of format bytes per SpMV, "
+                          f"> 4 x 126 MB), no flush" if flush is None else
+                          f"{bytes_model / 1e6:.0f} MB of format bytes per SpMV (< 4 x 126 MB L2): L2 flushed by a "
+                          f"512 MB read before every timed step and kernel rep, each timed on its own")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": f"spmv_{tag} {run_label} (rank 0 shard)", "bytes_per_launch": bytes_model,
+                     "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0,
+                     "reference_layout": {"variant": olabel, "frac": formats[olabel].get("frac"),
+                                          "gflops": formats[olabel].get("gflops")},
+                     "gather_bound": gather, "stream_gather_bound": stream_gather},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "exchange": exchange,
+        "clocks": clk,
+        "formats": formats,
+        "formats_relabelled": formats_run,
+        "configs": configs,
+        "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "canonicalize_first_call_s": t_canon_first,
+                       "to_csr_s": t_csr, "relabel_and_convert_s": t_relabel,
+                       "canonicalize_Mentries_per_s": raw_nnz / t_canon / 1e6},
+    }
+
+    # ---- N > 1: the other exchanges, same steps, for comparison ----
+    # (report the all-gather and the sparse exchange; p2p = our
+    # kernels over NVLink.)  These legs run LAST and under a watchdog: the
+    # headline line is complete at this point, so a comparison leg that hangs
+    # in a collective costs its own numbers, not the run -- every rank's timer
+    # thread fires after --compare-timeout-s, rank 0 prints the line with the
+    # legs finished so far, and the ranks exit 0.
+    if world > 1 and not args.no_compare:
+        import threading
+
+        def give_up():
+            exchange["comparison_timeout"] = f"a comparison leg exceeded {args.compare_timeout_s:.0f} s; legs finished before it are reported"
+            if rank == 0:
+                emit(line)
+            sys.stdout.flush()
+            sys.stderr.flush()
+            os._exit(0)
+
+        dog = threading.Timer(args.compare_timeout_s, give_up)
+        dog.daemon = True
+        dog.start()
+        others = ["allgatherv", "sparse"] + (["p2p"] if args.compare_p2p else [])
+        if native:  # the C-ABI driver ran the headline: time the torch one beside it
+            others[0] = "allgatherv-torch"
+        for other in others:
+            if other == mode:
+                continue
+            try:
+                pj = make_pi(other)
+                for _ in range(warmup):
+                    pj.step()
+                dist.barrier()
+                torch.cuda.synchronize()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                for _ in range(args.steps):
+                    pj.step()
+                ev1.record()
+                torch.cuda.synchronize()
+                tt = torch.tensor([ev0.elapsed_time(ev1) / 1e3], dtype=torch.float64, device=dev)
+                coll(dist.all_reduce, tt, op=dist.ReduceOp.MAX)
+                exchange[f"ms_per_step_{other}"] = float(tt.item()) / args.steps * 1e3
+                vol = vol or getattr(pj, "exchange_volume", None)
+                del pj
+            except Exception as exc:  # e.g. symmetric memory unavailable: report, keep the run
+                exchange[f"error_{other}"] = f"{type(exc).__name__}: {str(exc)[:160]}"
+        dog.cancel()
+        if vol:
+            exchange["rank0_volume_entries"] = vol
     if rank == 0:
-        emit({
-            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": warmup, "ms_per_step": t_loop / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "desc": w["desc"], "format": tag, "variant": label,
-                       "params": {k: v for k, v in kw.items() if k != "max_cells"}, "n": n,
-                       "nnz": nnz, "raw_draws_unique": raw_nnz, "parallelism": f"rowblock{world}",
-                       "balance": ("degree-sorted rows dealt round-robin to the rank blocks (nnz-balanced to "
-                                   "within one row)" if relabel and world > 1 else args.balance),
-                       "layout": ("degree-ordered shadow P A P^T (relabel.py), iterate x' = P x; the reference-layout "
-                                  "matrix serves the e2e calls" if relabel else "reference layout"),
-                       "step": (f"y=s*A x; ||y||^2 all-reduce; {exchange['mode']} exchange of x; s=1/||y||"
-                                if world > 1 else "y=s*A x; ||y||^2; s=1/||y||"),
-                       "eigenvalue_estimate": eig,
-                       "l2": (f"inputs larger than L2 ({bytes_model / 1e6:.0f} MB of format bytes per SpMV, "
-                              f"> 4 x 126 MB), no flush" if flush is None else
-                              f"{bytes_model / 1e6:.0f} MB of format bytes per SpMV (< 4 x 126 MB L2): L2 flushed by a "
-                              f"512 MB read before every timed step and kernel rep, each timed on its own")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": f"spmv_{tag} {run_label} (rank 0 shard)", "bytes_per_launch": bytes_model,
-                         "ms_per_launch": t_kernel * 1e3, "frac_of_8TBs": achieved / 8000.0,
-                         "reference_layout": {"variant": olabel, "frac": formats[olabel].get("frac"),
-                                              "gflops": formats[olabel].get("gflops")},
-                         "gather_bound": gather, "stream_gather_bound": stream_gather},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "exchange": exchange,
-            "clocks": clk,
-            "formats": formats,
-            "formats_relabelled": formats_run,
-            "configs": configs,
-            "conversion": {"rmat_gen_s": t_gen, "canonicalize_s": t_canon, "canonicalize_first_call_s": t_canon_first,
-                           "to_csr_s": t_csr, "relabel_and_convert_s": t_relabel,
-                           "canonicalize_Mentries_per_s": raw_nnz / t_canon / 1e6},
-        })
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -1045,6 +1065,10 @@ def main():
                     help="N > 1 row blocks: nnz-balanced (the config's) or nnz + 1.5 rows (see dist.cost_balanced_bounds)")
     ap.add_argument("--compare-p2p", action="store_true",
                     help="N > 1: also time the peer-memory exchange (symmetric memory) next to the default")
+    ap.add_argument("--no-compare", action="store_true",
+                    help="N > 1: skip the comparison legs (the other exchanges timed after the headline run)")
+    ap.add_argument("--compare-timeout-s", type=float, default=240.0,
+                    help="N > 1: watchdog over the comparison legs; when it fires the line is printed without them")
     ap.add_argument("--exchange", choices=["allgatherv", "sparse", "p2p"], default="allgatherv",
                     help="x exchange between row blocks (N > 1): the north-star all-gather of x (default), or "
                          "only the entries each shard reads; the other one is timed too and reported.  p2p "
