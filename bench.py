@@ -340,6 +340,7 @@ def run_configs(args, dev, peak, traffic):
         csr = sp.to_csr(a)
         del a
         recs = {}
+        built = {}  # label -> (tag, kw, on the shadow layout?)
         gpart = torch.empty(int(_lib.load().spmvb_gather_probe_threads()), dtype=torch.float64, device=dev)
         stream_ptr = torch.cuda.current_stream(dev).cuda_stream
 
@@ -372,6 +373,7 @@ def run_configs(args, dev, peak, traffic):
                 recs[label] = {"error": f"ConversionError: {str(exc)[:100]}"}
                 continue
             measure(label, lambda: sp.spmv(tag, m, x, out=y), spmv_bytes(tag, m), y, conv)
+            built[label] = (tag, kw, False)
             del m
         if "scale" in w:  # R-MAT: the run formats on the degree-ordered shadow layout
             torch.cuda.synchronize()
@@ -394,8 +396,8 @@ def run_configs(args, dev, peak, traffic):
                 fn = lambda: sp.spmv(tag, m, xp, out=yp)  # noqa: E731
                 fn()
                 measure(variant_label(tag, kw) + "-relabel", fn, spmv_bytes(tag, m), order.to_old(yp), conv)
+                built[variant_label(tag, kw) + "-relabel"] = (tag, kw, True)
                 del m
-            del order, shadow, xp, yp
         good = {k: v for k, v in recs.items() if "error" not in v}
         best = max(good, key=lambda k: good[k]["gflops"])
         # the same clock around a launch that only writes y: event + launch +
@@ -413,6 +415,45 @@ def run_configs(args, dev, peak, traffic):
                  "best_frac_of_stream_gather_ceiling": t_dot["-relabel" if best.endswith("-relabel") else ""] / t_best,
                  "all_within_tol": all(v["within_tol"] for v in good.values()),
                  "formats": recs}
+        # The best format again WITHOUT the flush: launches back to back over
+        # rotating distinct copies of the matrix, x and y whose total exceeds
+        # 4 x L2 (the same "inputs larger than L2" rule the C5 headline runs
+        # under), through prepared launches.  A flushed, isolated launch pays
+        # the event + launch + ramp of a cold GPU every time (launch_floor_us);
+        # back to back, each kernel starts while its predecessor drains
+        # (programmatic dependent launch), as in the power iteration.
+        btag, bkw, bshadow = built[best]
+        src, xv = (shadow, xp) if bshadow else (csr, x)
+        copies = max(2, int(-(-4 * 126e6 // b_best)) + 1)
+        ms = [sp.convert(btag, src, **bkw) for _ in range(copies)]
+        if btag in ("csr", "hyb"):
+            for m_ in ms:
+                m_.chunk_plan()
+        xs = [xv.clone() for _ in range(copies)]
+        ys = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(copies)]
+        calls = [sp.bind(btag, ms[i], xs[i], ys[i]) for i in range(copies)]
+        for c_ in calls:
+            c_()
+        rounds = max(3, int(2e-3 / t_best / copies))  # ~2 ms of launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(rounds):
+            for c_ in calls:
+                c_()
+        e1.record()
+        torch.cuda.synchronize()
+        t_rot = e0.elapsed_time(e1) / 1e3 / (rounds * copies)
+        same = all(torch.equal(ys[0], y_) for y_ in ys[1:])
+        entry["best_back_to_back"] = {
+            "us": t_rot * 1e6, "gflops": 2.0 * nnz / t_rot / 1e9, "frac": b_best / t_rot / 1e9 / peak,
+            "copies": copies, "launches": rounds * copies, "footprint_MB": copies * b_best / 1e6,
+            "bit_identical_across_copies": same,
+            "protocol": "prepared launches back to back over rotating distinct copies of matrix, x and y "
+                        "(total > 4 x 126 MB L2), one CUDA-event pair around all of them, no flush"}
+        del ms, xs, ys, calls
+        if "scale" in w:
+            del order, shadow, xp, yp
         if name == "C3":
             entry["power_iteration_100"] = c3_power_iteration(sp, spdist, csr, x, flush, nnz)
         out[name] = entry

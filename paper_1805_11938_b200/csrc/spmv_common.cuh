@@ -12,25 +12,62 @@ namespace spmvb {
 #define SPMVB_LDX_HOT 0  // > 0: columns >= this gather without L1 allocation (A/B knob)
 #endif
 #ifndef SPMVB_LDX_HOT_MODE
-#define SPMVB_LDX_HOT_MODE 0  // 0: cold no_allocate; 1: hot evict_last + cold evict_first
+// 0: cold no_allocate; 1: hot evict_last + cold evict_first (per lane: the
+// two loads diverge); 2: every gather evict_last; 3: every gather
+// evict_first; 4-6: ONE load per warp instruction, chosen by a vote -- when
+// at least SPMVB_LDX_VOTE active lanes gather a cold column the whole warp
+// uses evict_first (4) / no_allocate (5) / the default policy (6), else
+// evict_last (4, 6) / the default (5).  All A/B knobs; every variant was
+// slower than the plain __ldg (profiles/r02_l1_hot_split_ab.txt,
+// profiles/r02_l1_vote_ab.txt).
+#define SPMVB_LDX_HOT_MODE 0
 #endif
-__device__ __forceinline__ double ldx(const double* __restrict__ x, int32_t j) {
-#if SPMVB_LDX_HOT > 0
+#ifndef SPMVB_LDX_VOTE
+#define SPMVB_LDX_VOTE 24
+#endif
+__device__ __forceinline__ double ldx_el(const double* p) {
   double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldx_ef(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldx_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldx(const double* __restrict__ x, int32_t j) {
+#if SPMVB_LDX_HOT_MODE == 2
+  return ldx_el(x + j);
+#elif SPMVB_LDX_HOT_MODE == 3
+  return ldx_ef(x + j);
+#elif SPMVB_LDX_HOT > 0 && SPMVB_LDX_HOT_MODE >= 4
+  const unsigned am = __activemask();
+  const bool cold = __popc(__ballot_sync(am, j >= SPMVB_LDX_HOT)) >= min(SPMVB_LDX_VOTE, __popc(am));
+#if SPMVB_LDX_HOT_MODE == 4
+  return cold ? ldx_ef(x + j) : ldx_el(x + j);
+#elif SPMVB_LDX_HOT_MODE == 5
+  return cold ? ldx_na(x + j) : __ldg(x + j);
+#else
+  return cold ? __ldg(x + j) : ldx_el(x + j);
+#endif
+#elif SPMVB_LDX_HOT > 0
   if (j < SPMVB_LDX_HOT) {
 #if SPMVB_LDX_HOT_MODE == 1
-    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
+    return ldx_el(x + j);
 #else
-    v = __ldg(x + j);
-#endif
-  } else {
-#if SPMVB_LDX_HOT_MODE == 1
-    asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
-#else
-    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
+    return __ldg(x + j);
 #endif
   }
-  return v;
+#if SPMVB_LDX_HOT_MODE == 1
+  return ldx_ef(x + j);
+#else
+  return ldx_na(x + j);
+#endif
 #elif SPMVB_LDX_NOALLOC
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(x + j));
