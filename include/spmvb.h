@@ -210,6 +210,26 @@ int spmvb_spmv_hyb(int64_t n_rows, int64_t k, const int32_t* ell_idx, const doub
                    int64_t n_nz, const int32_t* chunk_row, int32_t* carry_row, double* carry_val, const double* x,
                    double* y, const double* scale, void* stream);
 
+/* Reference-order ("bit-parity") SpMV (csrc/spmv_exact.cu): the reference's
+ * own summation orders, so y equals spmvkit's result (workers = 1) bit for
+ * bit, where the fast kernels above meet the 1e-12 (|A||x|) tolerance in a
+ * different fixed order.  CSR: y_r = p_first + numpy-pairwise(rest)
+ * (np.add.reduceat, kernels.py:84).  CSR5: the same per row piece inside each
+ * tile, pieces added in ascending tile order from 0.0 (kernels.py:161-173);
+ * indices/data in CSR5 stored order.  HYB: the sequential ELL recurrence, then
+ * + the row's tail entries summed sequentially from 0.0 (np.bincount,
+ * kernels.py:186-198).  ELL and SELL (every slice on the thread-per-row path)
+ * already are the reference recurrence.  A verification mode: a thread per
+ * row, a CTA per row longer than 256 entries. */
+int spmvb_spmv_csr_exact(int64_t n_rows, int64_t nnz, const int32_t* ptr, const int32_t* col, const double* val,
+                         const double* x, double* y, const double* scale, void* stream);
+int spmvb_spmv_csr5_exact(int64_t n_rows, int64_t nnz, const int32_t* ptr, int omega, int sigma,
+                          const int32_t* indices, const double* data, const double* x, double* y,
+                          const double* scale, void* stream);
+int spmvb_spmv_hyb_exact(int64_t n_rows, int64_t k, const int32_t* ell_idx, const double* ell_val, int64_t tail_nnz,
+                         const int32_t* tail_ptr, const int32_t* tail_col, const double* tail_val, const double* x,
+                         double* y, const double* scale, void* stream);
+
 /* spmv_csr5 (kernels.py:139-174). nonempty_rows may be NULL when every row is
  * non-empty, or when the non-empty rows are exactly the prefix
  * [0, n_nonempty) (n_nonempty < n_rows: the empty tail is zeroed by plain

@@ -79,6 +79,9 @@ SIGNATURES: dict[str, tuple] = {
         c_int,
         [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp],
     ),
+    "spmvb_spmv_csr_exact": (c_int, [c_i64, c_i64, vp, vp, vp, vp, vp, vp, vp]),
+    "spmvb_spmv_csr5_exact": (c_int, [c_i64, c_i64, vp, c_int, c_int, vp, vp, vp, vp, vp, vp]),
+    "spmvb_spmv_hyb_exact": (c_int, [c_i64, c_i64, vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp]),
     "spmvb_csr5_pack_flags": (c_int, [c_i64, vp, vp, vp]),
     "spmvb_spmv_csr5": (
         c_int,

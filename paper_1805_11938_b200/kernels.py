@@ -12,7 +12,13 @@ traffic); a CPU tensor gives a CPU tensor (pinned in -> pinned out, copies
 on the current stream); anything else (numpy, list) is coerced like the
 reference (``np.asarray(x, float64).ravel()``) and returns a numpy array.
 Keyword-only extensions: ``out=`` (device output buffer) and ``scale=`` (a
-device scalar multiplying every row result; power iteration uses it).
+device scalar multiplying every row result; power iteration uses it) and
+``exact=True``: the reference's own summation order, so y equals spmvkit's
+result (``workers=1``) bit for bit -- CSR / CSR5 / HYB run the reference-order
+kernels of csrc/spmv_exact.cu (numpy's reduceat / bincount orders), SELL keeps
+every slice on its thread-per-row path, ELL is unchanged; a verification mode,
+slower than the default kernels, whose results meet the 1e-12 (|A||x|)
+tolerance in a different fixed order.
 Repeated calls are bit-identical (no floating-point atomics).
 """
 
@@ -123,8 +129,15 @@ def _scratch_csr(m: CsrMatrix):
     return m.chunk_plan().scratch(m.device)
 
 
-def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = A x for CSR via the chunked kernel (kernels.py:76-95)."""
+def spmv_csr(m: CsrMatrix, x, workers: int = 1, *, out=None, scale=None, exact: bool = False):
+    """y = A x for CSR via the chunked kernel (kernels.py:76-95);
+    ``exact=True``: y_r = p_first + pairwise(rest), numpy's reduceat order."""
+    if exact:
+        def launch_exact(xd, y, sp, s):
+            check(LIB.spmvb_spmv_csr_exact(m.n_rows, m.nnz, ptr(m.ptr), ptr(m.indices), ptr(m.data), ptr(xd), ptr(y),
+                                           sp, s))
+
+        return _run(m, x, out, scale, launch_exact)
     m.chunk_plan()
 
     def launch(xd, y, sp, s):
@@ -154,13 +167,20 @@ def _scratch_csr5(m: Csr5Matrix):
     return torch.empty(max(m.num_tiles, 1), dtype=torch.float64, device=m.device)
 
 
-def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None, ranges: int = 16):
+def spmv_csr5(m: Csr5Matrix, x, workers: int = 1, *, out=None, scale=None, ranges: int = 16, exact: bool = False):
     """y = A x for CSR5: per-tile segmented sums + ordered carry fix-up (kernels.py:139-174).
+    ``exact=True``: per-tile reduceat sums added in ascending tile order, as the reference.
 
     Host x with a host (or no) ``out`` runs the streamed host-buffer entry
     point: x is copied in once, then ``ranges`` tile ranges compute in order
     while each range's finished rows of y are copied back on a second stream.
     """
+    if exact:
+        def launch_exact(xd, y, sp, s):
+            check(LIB.spmvb_spmv_csr5_exact(m.n_rows, m.nnz, ptr(m.ptr), m.omega, m.sigma, ptr(m.indices),
+                                            ptr(m.data), ptr(xd), ptr(y), sp, s))
+
+        return _run(m, x, out, scale, launch_exact)
     if _is_host(x) and (out is None or _is_host(out)):
         return _spmv_csr5_host(m, x, out, scale, ranges)
 
@@ -264,8 +284,9 @@ def _args_ell(m: EllMatrix, xd, y, sp, scratch):
     return "spmvb_spmv_ell", (m.n_rows, m.n_cols, m.k, ptr(m.grid_indices), ptr(m.grid_data), ptr(xd), ptr(y), sp)
 
 
-def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = A x for ELL, sequential over the k slots (kernels.py:98-116)."""
+def spmv_ell(m: EllMatrix, x, workers: int = 1, *, out=None, scale=None, exact: bool = False):
+    """y = A x for ELL, sequential over the k slots (kernels.py:98-116): the
+    reference recurrence, so ``exact`` changes nothing."""
 
     def launch(xd, y, sp, s):
         name, args = _args_ell(m, xd, y, sp, None)
@@ -282,8 +303,18 @@ def _args_sell(m: SellMatrix, xd, y, sp, scratch):
                                wide_cols, tail_from, max_narrow, ptr(xd), ptr(y), sp)
 
 
-def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = A x for SELL / SELL-C-sigma, scattered through perm (kernels.py:119-136)."""
+def spmv_sell(m: SellMatrix, x, workers: int = 1, *, out=None, scale=None, exact: bool = False):
+    """y = A x for SELL / SELL-C-sigma, scattered through perm (kernels.py:119-136).
+    ``exact=True``: slices wider than the wide threshold also run a thread per
+    row (the reference recurrence) instead of being summed in pieces."""
+    if exact:
+        def launch_exact(xd, y, sp, s):
+            perm = m.perm if m.sigma > 0 else None
+            check(LIB.spmvb_spmv_sell(m.n_rows, m.c, ptr(m.widths), ptr(m.slice_off), ptr(perm), ptr(m.flat_indices),
+                                      ptr(m.flat_data), None, 0, None, 0, None, 0, 1 << 62, m.n_rows, -1, ptr(xd),
+                                      ptr(y), sp, s))
+
+        return _run(m, x, out, scale, launch_exact)
     m.wide_plan()
 
     def launch(xd, y, sp, s):
@@ -329,8 +360,17 @@ def _scratch_hyb(m: HybMatrix):
     return m.chunk_plan().scratch(m.device)
 
 
-def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None):
-    """y = ELL part + COO tail (kernels.py:177-199), one fused kernel."""
+def spmv_hyb(m: HybMatrix, x, workers: int = 1, *, out=None, scale=None, exact: bool = False):
+    """y = ELL part + COO tail (kernels.py:177-199), one fused kernel.
+    ``exact=True``: ell_r + (the row's tail entries summed sequentially from
+    0.0), the reference's spmv_ell + bincount order."""
+    if exact:
+        def launch_exact(xd, y, sp, s):
+            t = m.coo_tail
+            check(LIB.spmvb_spmv_hyb_exact(m.n_rows, m.k, ptr(m.ell.grid_indices), ptr(m.ell.grid_data), t.nnz,
+                                           ptr(m.tail_ptr), ptr(t.col), ptr(t.data), ptr(xd), ptr(y), sp, s))
+
+        return _run(m, x, out, scale, launch_exact)
     m.chunk_plan()
 
     def launch(xd, y, sp, s):

@@ -79,6 +79,8 @@ def test_config_parity(sp, name):
     m = sp.to_csr(a)
     assert np.array_equal(h(m.ptr), ptr)
     check_within(sp.spmv("csr", m, xd), ref, bound)
+    # exact=True: the reference's own summation order, bit for bit (csrc/spmv_exact.cu)
+    assert h(sp.spmv("csr", m, xd, exact=True)).tobytes() == port.spmv_csr(ptr, ind, dat, n, x).tobytes()
 
     for om, sg in [(4, 16), (32, 16), (32, 8)]:
         m5 = sp.to_csr5(m, om, sg)
@@ -89,6 +91,8 @@ def test_config_parity(sp, name):
         y5 = sp.spmv("csr5", m5, xd)
         check_within(y5, ref, bound)
         assert h(sp.spmv("csr5", m5, xd)).tobytes() == h(y5).tobytes()
+        if sg == 16:
+            assert h(sp.spmv("csr5", m5, xd, exact=True)).tobytes() == port.spmv_csr5(o5, n, x).tobytes()
 
     try:
         k, gi, gd, cnt = port.to_ell(ptr, ind, dat, n)
@@ -120,6 +124,7 @@ def test_config_parity(sp, name):
             assert h(ys).tobytes() == port.spmv_sell(so, n, x).tobytes()
         else:  # wide power-law slices are split across a CTA (SPMVB_SELL_WIDE_COLS)
             check_within(ys, ref, bound)
+            assert h(sp.spmv("sell", ms, xd, exact=True)).tobytes() == port.spmv_sell(so, n, x).tobytes()
 
     K, hi, hd, hn, tail = port.to_hyb(row, col, val, n)
     mh = sp.to_hyb(m)
@@ -129,6 +134,7 @@ def test_config_parity(sp, name):
     assert np.array_equal(h(mh.coo_tail.row), tail[0]) and np.array_equal(h(mh.coo_tail.col), tail[1])
     assert h(mh.coo_tail.data).tobytes() == tail[2].tobytes()
     check_within(sp.spmv("hyb", mh, xd), ref, bound)
+    assert h(sp.spmv("hyb", mh, xd, exact=True)).tobytes() == port.spmv_hyb(K, hi, hd, tail, n, x).tobytes()
 
     f = sp.extract_features(m)
     assert f.as_array().tobytes() == np.array(port.extract_features(row, n, n)).tobytes()

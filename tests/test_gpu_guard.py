@@ -20,6 +20,7 @@ import pytest
 import torch
 
 import test_gpu_dispatch as tdisp
+import test_gpu_exact as texact
 import test_gpu_p2p as tp2p
 import test_gpu_parity as tpar
 import test_gpu_relabel as trel
@@ -159,6 +160,16 @@ def test_guarded_relabel(guarded, sp):
     trel.test_prefix_csr5_spmv(sp, 32, 16)
     trel.test_prefix_csr5_spmv(sp, 4, 16)
     trel.test_relabelled_power_iteration_matches_oracle(sp)
+
+
+def test_guarded_exact_mode(guarded, sp, golden):
+    """The reference-order kernels (csrc/spmv_exact.cu): golden cases, the
+    CTA-per-long-row paths and the containers under guard bands."""
+    texact.test_exact_equals_the_reference_outputs(sp, golden)
+    guarded.check()
+    texact.test_exact_long_rows_against_the_oracle(sp)
+    guarded.check()
+    texact.test_exact_scale_containers_and_repeat(sp)
 
 
 def test_guard_detects_an_overrun(guarded, sp):
