@@ -249,3 +249,54 @@ def test_c5_shadow_layout_spmv_sampled_rows(c5, y_ref, tag, kw):
     assert np.all(err <= TOL * bound), (tag, float(np.max(err / np.maximum(bound, 1e-300))))
     del rm, y, order
     torch.cuda.empty_cache()
+
+
+def test_c5_exact_mode_sampled_rows(c5, host):
+    """exact=True at C5: y at the sampled rows bit-identical to the
+    reference's summation orders evaluated on the host copies of those rows
+    -- CSR (reduceat: first + pairwise(rest)), CSR5 omega 32 sigma 16 (the
+    row's pieces inside each GLOBAL tile, reduceat each, added in tile order)
+    and HYB (the sequential ELL part of the first K entries + the bincount
+    sum of the rest)."""
+    sp, m, hx = c5["sp"], c5["m"], c5["hx"]
+    rows = host["sampled"]
+    rd = torch.from_numpy(rows).cuda()
+    ptr, ind, dat = _rows_of(host, rows)
+    cnt = np.diff(ptr)
+    live = np.nonzero(cnt)[0]
+    prod = dat * hx[ind]
+    # CSR
+    want = np.zeros(rows.size)
+    want[live] = np.add.reduceat(prod, ptr[:-1][live])
+    got = h(sp.spmv("csr", m, c5["x"], exact=True)[rd])
+    assert got.tobytes() == want.tobytes()
+    # CSR5: cut every sampled row at the global tile boundaries
+    tile = 32 * 16
+    dptr = h(m.ptr).astype(np.int64)
+    g0 = dptr[rows]                                     # global CSR position of each row's first entry
+    gpos = np.repeat(g0 - ptr[:-1], cnt) + np.arange(prod.size)
+    start = np.zeros(prod.size, dtype=bool)
+    start[ptr[:-1][live]] = True
+    start |= gpos % tile == 0
+    starts = np.nonzero(start)[0]
+    sums = np.add.reduceat(prod, starts)
+    seg_row = np.searchsorted(ptr, starts, side="right") - 1
+    want5 = np.zeros(rows.size)
+    np.add.at(want5, seg_row, sums)                     # in order: ((0 + s_1) + s_2) + ...
+    m5 = sp.to_csr5(m, 32, 16)
+    got5 = h(sp.spmv("csr5", m5, c5["x"], exact=True)[rd])
+    del m5
+    torch.cuda.empty_cache()
+    assert got5.tobytes() == want5.tobytes()
+    assert (cnt > 3 * tile).any() and want5.tobytes() != want.tobytes()  # rows spanning tiles: the orders differ
+    # HYB
+    mh = sp.to_hyb(m)
+    K = mh.k
+    ec = np.minimum(cnt, K)
+    keep = (np.arange(ind.size) - np.repeat(ptr[:-1], cnt)) < K
+    ei, ed = port._grids(rows.size, K, ec, np.concatenate([[0], np.cumsum(ec)]), ind[keep], dat[keep], 1 << 62)
+    wanth = port.spmv_ell(K, ei, ed, hx)
+    local = np.repeat(np.arange(rows.size), cnt)
+    wanth += np.bincount(local[~keep], weights=prod[~keep], minlength=rows.size)
+    goth = h(sp.spmv("hyb", mh, c5["x"], exact=True)[rd])
+    assert goth.tobytes() == wanth.tobytes()
