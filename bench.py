@@ -454,6 +454,16 @@ def run_configs(args, dev, peak, traffic):
         del ms, xs, ys, calls
         if "scale" in w:
             del order, shadow, xp, yp
+        # the shipped B200 selector (features on the GPU -> the reference's tree
+        # trained on B200 labels): its pick among the reference-layout variants
+        # measured above, against the fastest of them
+        pick = sp.predict(sp.default_model(), sp.extract_features(csr)).value
+        pick_label = {"csr": "csr", "csr5": "csr5-w32s16", "ell": "ell", "sell": "sell-c32s1024", "hyb": "hyb"}[pick]
+        plain = {k: v for k, v in good.items() if not k.endswith("-relabel")}
+        fastest = min(plain, key=lambda k: plain[k]["us"])
+        entry["selector"] = {"predicted": pick, "variant": pick_label, "fastest_reference_layout": fastest,
+                             "speed_vs_fastest": (plain[fastest]["us"] / plain[pick_label]["us"]
+                                                  if pick_label in plain else 0.0)}
         if name == "C3":
             entry["power_iteration_100"] = c3_power_iteration(sp, spdist, csr, x, flush, nnz)
         out[name] = entry

@@ -29,7 +29,11 @@ from .features import (  # noqa: E402
     apply_scaling,
     extract_extra_features,
     extract_features,
+    features_from_line,
+    features_to_line,
     fit_scaling,
+    read_features,
+    write_features,
 )
 from .formats import (  # noqa: E402
     DEFAULT_MAX_GRID_CELLS,
@@ -73,11 +77,14 @@ from .kernels import (  # noqa: E402
 )
 from .relabel import DegreeOrder, RelabelledMatrix, power_iteration  # noqa: E402
 from .model import (  # noqa: E402
+    B200_SELECTOR_PARAMS,
     DecisionTreeModel,
     ModelIOError,
+    default_model,
     load_model,
     predict,
     select_format,
+    select_format_b200,
     select_format_measured,
 )
 

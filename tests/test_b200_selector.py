@@ -1,0 +1,84 @@
+"""The shipped B200 format selector (paper_1805_11938_b200/data/).
+
+The model was trained by the REFERENCE's unchanged train_tree on labels
+measured on a B200 (scripts/b200_labels.py -> scripts/train_b200_model.py,
+which also recorded spmvkit.predict and spmvkit.best_labels for every
+corpus matrix in tests/golden/b200_selector_predictions.json).  Here, on
+CPU: our loader and tree descent give the reference's predictions on all
+222 matrices, our record reader and best_labels give the reference's labels
+from the shipped B200 records, and the feature-file reader round-trips.
+"""
+
+from __future__ import annotations
+
+import io
+import json
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+DATA = ROOT / "paper_1805_11938_b200" / "data"
+PINNED = json.loads((ROOT / "tests" / "golden" / "b200_selector_predictions.json").read_text())
+
+
+def test_shipped_model_predicts_as_the_reference_did():
+    import paper_1805_11938_b200 as sp
+
+    model = sp.default_model()
+    assert model is sp.default_model() and len(model.nodes) > 10
+    feats = sp.read_features(DATA / "b200_features.txt")
+    assert len(feats) == len(PINNED["predictions"]) >= 200
+    for mid, f in feats:
+        assert sp.predict(model, f).value == PINNED["predictions"][mid], mid
+    hit = sum(PINNED["predictions"][mid] == PINNED["labels"][mid] for mid, _ in feats)
+    assert hit / len(feats) > 0.8  # training-set accuracy of the shipped tree
+
+
+def test_shipped_records_give_the_reference_labels():
+    from paper_1805_11938_b200 import harness
+
+    records = harness.read_records(DATA / "b200_records.txt")
+    assert len(records) == 5 * len(PINNED["labels"])
+    labels = harness.best_labels(records)
+    assert {k: v.value for k, v in labels.items()} == PINNED["labels"]
+    assert set(v.value for v in labels.values()) == {"csr", "csr5", "ell", "sell", "hyb"}  # every format wins somewhere
+    times = harness.times_by_matrix(records)
+    assert all(per[labels[mid]] == min(per.values()) for mid, per in times.items())
+
+
+def test_feature_file_round_trip():
+    import paper_1805_11938_b200 as sp
+
+    text = (DATA / "b200_features.txt").read_text()
+    feats = sp.read_features(io.StringIO(text))
+    out = io.StringIO()
+    sp.write_features(feats, out)
+    assert out.getvalue() == text
+    with pytest.raises(ValueError, match="bad feature line"):
+        sp.features_from_line("matrix_id:x n_rows:3")
+
+
+@pytest.mark.gpu
+def test_select_format_b200_on_the_configs():
+    """GPU: features -> shipped tree -> conversion, on C1 and a C4-like R-MAT;
+    the chosen format's y is within tolerance of the sequential oracle and
+    its SpMV time within 1.5x of the measured-best candidate."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1805_11938_b200 as sp
+    from paper_1805_11938_b200 import synth
+
+    for a, expect in ((synth.host_coo("C1"), {"ell", "hyb", "sell"}),
+                      (synth.rmat_coo(19, 10, 7), {"csr", "csr5", "sell", "hyb"})):
+        tag, m = sp.select_format_b200(a)
+        assert tag.value in expect, tag
+        x = synth.uniform_vector(a.n_cols, 5)
+        y = sp.spmv(tag, m, x)
+        ref = sp.dense_spmv_oracle(a, x)
+        bound = sp.dense_spmv_oracle(sp.CooMatrix(a.n_rows, a.n_cols, a.row, a.col, a.data.abs()), x.abs())
+        assert bool(((y - ref).abs() <= 1e-12 * bound).all())
+        _, _, times = sp.select_format_measured(a, reps=50)
+        assert times[tag] <= 1.5 * min(times.values()), (tag, times)
