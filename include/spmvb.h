@@ -83,6 +83,16 @@ int spmvb_mm_parse(const char* text, int64_t len, int pattern, int symmetric, in
                    int64_t declared, int64_t cap, int64_t* row_out, int64_t* col_out, double* val_out, int64_t* n_out,
                    int64_t* err_line, int64_t* err_ij, int n_threads);
 
+/* write_matrix_market entry formatter (coo.py:266-278), host code,
+ * multithreaded: one "<row+1> <col+1> <value:.17g>\n" line per entry, the
+ * text Python's f"{v:.17g}" produces.  _begin formats into a plan and returns
+ * the text length; _finish copies it into `out` (len bytes; NULL = discard)
+ * and frees the plan.  The banner and the size line are the caller's. */
+typedef struct spmvb_mm_text spmvb_mm_text;
+int spmvb_mm_format_begin(const int64_t* row, const int64_t* col, const double* val, int64_t nnz, int n_threads,
+                          spmvb_mm_text** plan_out, int64_t* len_out);
+int spmvb_mm_format_finish(spmvb_mm_text* plan, char* out);
+
 /* row_nnz_histogram (coo.py:144-146) on canonical (row-sorted) COO. */
 int spmvb_row_nnz_histogram(const int32_t* row, int64_t nnz, int64_t n_rows, int64_t* counts_out,
                             void* stream);

@@ -49,9 +49,11 @@ SIGNATURES: dict[str, tuple] = {
     "spmvb_canonicalize_begin": (c_int, [vp, vp, c_int, vp, c_i64, c_i64, c_i64, P_vp, P_i64, P_i64, vp]),
     "spmvb_canonicalize_finish": (c_int, [vp, vp, vp, vp, vp]),
     "spmvb_canonicalize_free": (None, [vp]),
+    "spmvb_mm_format_begin": (c_int, [vp, vp, vp, c_i64, c_int, P_vp, P_i64]),
+    "spmvb_mm_format_finish": (c_int, [vp, vp]),
     "spmvb_mm_parse": (
         c_int,
-        [ctypes.c_char_p, c_i64, c_int, c_int, c_i64, c_i64, c_i64, c_i64, vp, vp, vp, P_i64, P_i64, P_i64, c_int],
+        [vp, c_i64, c_int, c_int, c_i64, c_i64, c_i64, c_i64, vp, vp, vp, P_i64, P_i64, P_i64, c_int],
     ),
     "spmvb_row_nnz_histogram": (c_int, [vp, c_i64, c_i64, vp, vp]),
     "spmvb_spmv_sequential": (c_int, [c_i64, vp, vp, vp, vp, vp, vp]),

@@ -251,3 +251,100 @@ extern "C" int spmvb_mm_parse(const char* text, int64_t len, int pattern, int sy
   *n_out = n;
   return MM_OK;
 }
+
+// ---------------------------------------------------------------------------
+// write_matrix_market entry formatter (coo.py:266-278): one line per entry,
+// "<row+1> <col+1> <value:.17g>\n", formatted by n_threads threads into
+// per-thread buffers; _begin returns the total length, _finish copies the
+// text into the caller's buffer and frees the plan.  std::to_chars(general,
+// 17) is printf's %.17g, which is Python's format(v, ".17g") for every finite
+// double; non-finite values are spelled as Python spells them (inf, -inf,
+// nan).
+// ---------------------------------------------------------------------------
+#include <cmath>
+
+struct spmvb_mm_text {
+  std::vector<std::vector<char>> parts;
+};
+
+namespace {
+
+inline char* put_int(char* p, int64_t v) { return std::to_chars(p, p + 24, v).ptr; }
+
+inline char* put_real(char* p, double v) {
+  if (std::isnan(v)) {
+    std::memcpy(p, "nan", 3);
+    return p + 3;
+  }
+  if (std::isinf(v)) {
+    const char* s = v < 0 ? "-inf" : "inf";
+    const size_t n = std::strlen(s);
+    std::memcpy(p, s, n);
+    return p + n;
+  }
+  return std::to_chars(p, p + 40, v, std::chars_format::general, 17).ptr;
+}
+
+}  // namespace
+
+extern "C" int spmvb_mm_format_begin(const int64_t* row, const int64_t* col, const double* val, int64_t nnz,
+                                     int n_threads, spmvb_mm_text** plan_out, int64_t* len_out) {
+  if (!plan_out || !len_out || nnz < 0 || (nnz > 0 && (!row || !col || !val))) return 1;
+  if (n_threads < 1) n_threads = 1;
+  if (nnz < (1 << 16)) n_threads = 1;
+  auto* plan = new (std::nothrow) spmvb_mm_text;
+  if (!plan) return 5;
+  plan->parts.resize(n_threads);
+  bool failed = false;
+  auto work = [&](int t) {
+    const int64_t lo = nnz * t / n_threads, hi = nnz * (t + 1) / n_threads;
+    try {
+      std::vector<char>& out = plan->parts[t];
+      out.resize(static_cast<size_t>(hi - lo) * 72 + 8);  // 2 x 20 digits + 26 for the value + separators
+      char* p = out.data();
+      for (int64_t k = lo; k < hi; ++k) {
+        p = put_int(p, row[k] + 1);
+        *p++ = ' ';
+        p = put_int(p, col[k] + 1);
+        *p++ = ' ';
+        p = put_real(p, val[k]);
+        *p++ = '\n';
+      }
+      out.resize(static_cast<size_t>(p - out.data()));
+    } catch (...) {
+      failed = true;
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    for (int t = 1; t < n_threads; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+  }
+  if (failed) {
+    delete plan;
+    return 5;
+  }
+  int64_t total = 0;
+  for (auto& part : plan->parts) total += static_cast<int64_t>(part.size());
+  *plan_out = plan;
+  *len_out = total;
+  return 0;
+}
+
+extern "C" int spmvb_mm_format_finish(spmvb_mm_text* plan, char* out) {
+  if (!plan) return 1;
+  if (out) {
+    std::vector<std::thread> th;
+    size_t off = 0;
+    for (auto& part : plan->parts) {
+      char* dst = out + off;
+      const std::vector<char>* src = &part;
+      th.emplace_back([dst, src] { std::memcpy(dst, src->data(), src->size()); });
+      off += part.size();
+    }
+    for (auto& x : th) x.join();
+  }
+  delete plan;
+  return 0;
+}
