@@ -168,10 +168,16 @@ inline unsigned grid_for(int64_t n, int block, int64_t cap = (1ll << 30)) {
 // SELL wide slices (width > SPMVB_SELL_WIDE_COLS, at most 128 rows) are
 // processed in pieces of about SELL_PIECE_CELLS cells (whole columns), one
 // CTA per piece, by the SpMV and by the fill (spmvb_sell_wide_plan).
-constexpr int64_t SELL_PIECE_CELLS = 32768;
+#ifndef SPMVB_SELL_PIECE_MIN_COLS
+#define SPMVB_SELL_PIECE_MIN_COLS 256
+#endif
+#ifndef SPMVB_SELL_PIECE_CELLS
+#define SPMVB_SELL_PIECE_CELLS 32768
+#endif
+constexpr int64_t SELL_PIECE_CELLS = SPMVB_SELL_PIECE_CELLS;
 __host__ __device__ __forceinline__ int64_t sell_piece_cols(int rows_s) {
   const int64_t pc = SELL_PIECE_CELLS / rows_s;
-  return pc < 256 ? 256 : pc;
+  return pc < SPMVB_SELL_PIECE_MIN_COLS ? SPMVB_SELL_PIECE_MIN_COLS : pc;
 }
 __host__ __device__ __forceinline__ int sell_rows(int64_t sl, int64_t c, int64_t n_rows) {
   return static_cast<int>((sl + 1) * c <= n_rows ? c : n_rows - sl * c);
