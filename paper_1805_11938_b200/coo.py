@@ -443,7 +443,7 @@ def write_matrix_market(a, dest) -> None:
             fh.write(body)
 
 
-def _format_entries(r, c, d) -> bytes:
+def _format_entries(r, c, d) -> bytearray:
     """The entry lines ``"<i+1> <j+1> <v:.17g>\\n"`` of write_matrix_market,
     formatted by the native multithreaded formatter (csrc/mmio.cpp); byte
     for byte what the reference's Python expression produces."""
@@ -460,4 +460,4 @@ def _format_entries(r, c, d) -> bytes:
     buf = (ctypes.c_char * len(out)).from_buffer(out) if out else None
     LIB.spmvb_mm_format_finish(plan, ctypes.addressof(buf) if buf is not None else None)
     del buf
-    return bytes(out) if len(out) < (1 << 20) else out
+    return out
