@@ -8,6 +8,7 @@ cross_validate (k = 5, 3 repeats, with the per-format runtimes for the
 performance ratio) and train_tree + save_model on all samples.
 
     python scripts/train_b200_model.py [--src gpurun_out]
+    python scripts/train_b200_model.py --src paper_1805_11938_b200/data   # regenerate from the shipped records
 
 Writes
     paper_1805_11938_b200/data/b200_selector.model   the shipped model (spmvkit-model v1 text)
@@ -55,8 +56,9 @@ def main():
     data = ROOT / "paper_1805_11938_b200" / "data"
     data.mkdir(exist_ok=True)
     rmodel.save_model(model, data / "b200_selector.model")
-    shutil.copy(src / "b200_records.txt", data / "b200_records.txt")
-    shutil.copy(src / "b200_features.txt", data / "b200_features.txt")
+    if src.resolve() != data.resolve():  # --src paper_1805_11938_b200/data regenerates the model from the shipped files
+        shutil.copy(src / "b200_records.txt", data / "b200_records.txt")
+        shutil.copy(src / "b200_features.txt", data / "b200_features.txt")
     preds = {s.matrix_id: rmodel.predict(model, s.features).value for s in samples}
     (ROOT / "tests" / "golden" / "b200_selector_predictions.json").write_text(
         json.dumps({"labels": {k: v.value for k, v in labels.items()}, "predictions": preds}, indent=0, sort_keys=True))
@@ -78,6 +80,8 @@ def main():
     train_acc = float(np.mean([preds[s.matrix_id] == s.label.value for s in samples]))
     fam = {}
     corpus = src / "b200_corpus.jsonl"
+    if not corpus.exists():
+        corpus = ROOT / "profiles" / "r02_b200_corpus.jsonl"
     if corpus.exists():
         for line in corpus.read_text().splitlines():
             m = json.loads(line)
