@@ -34,7 +34,7 @@ def main():
         x = synth.uniform_vector(csr.n_cols, w["x_seed"], device=dev)
         order = DegreeOrder(csr)
         csr, x = order.matrix(csr), order.to_new(x)
-        for sigma in (8, 16):
+        for sigma in tuple(int(v) for v in os.environ.get("CSR5_AB_SIGMAS", "8,16").split(",")):
             m = sp.to_csr5(csr, 32, sigma)
             y = torch.empty(m.n_rows, dtype=torch.float64, device=dev)
             fn = lambda: sp.spmv("csr5", m, x, out=y)  # noqa: E731
