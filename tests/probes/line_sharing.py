@@ -1,8 +1,8 @@
 """Distinct 128-byte x lines touched by one 32-lane gather instruction for an
 R-MAT matrix under three lane layouts (striped, 8 per lane, CSR5 sigma=16),
-with original and degree-relabelled columns.  python scripts/line_sharing.py 21 10"""
+with original and degree-relabelled columns.  python tests/probes/line_sharing.py 21 10"""
 import numpy as np, sys
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('pathlib').Path(__file__).resolve().parents[2].as_posix())
 from oracle import synth_ref
 scale, ef = int(sys.argv[1]), int(sys.argv[2])
 r, c, v = synth_ref.rmat(scale, ef, 104)

@@ -1,9 +1,9 @@
 """Distinct 128-byte x lines per 32-lane gather for the rows of the wide SELL
 slices of the degree-ordered R-MAT matrix, under two traversals: 32 rows at
 one slot (the current k_sell_wide_part) and one row at 32 consecutive slots.
-    python scripts/line_sharing_wide.py 21 10 104 > profiles/r02_line_sharing_wide.txt"""
+    python tests/probes/line_sharing_wide.py 21 10 104 > profiles/r02_line_sharing_wide.txt"""
 import sys, numpy as np
-sys.path.insert(0,'/root/repo')
+sys.path.insert(0, __import__('pathlib').Path(__file__).resolve().parents[2].as_posix())
 from oracle import cpu_baseline
 scale, ef, seed = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 ptr, ind, dat = cpu_baseline.rmat_full_csr(scale, ef, seed)
